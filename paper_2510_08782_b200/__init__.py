@@ -1,0 +1,224 @@
+"""paper_2510_08782_b200 — B200-native GA-NGMRES for transport-constrained optimisation.
+
+Thin Python binding of the C ABI in ``include/topt.h`` (libtopt.so, hand-written
+sm_100a CUDA kernels).  PyTorch supplies device memory, streams and process
+groups only; every step of the hot path runs in the library's kernels.  Names
+follow PAPER.md (arXiv 2510.08782): m0, m1, v, alpha, nt, g, s, obj, GA-NGMRES
+(w; sigma, tau).
+
+Import fails loudly when the library is missing (no CPU fallback).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import LIB, Params, Report, ToptError, check
+
+__all__ = ["Topt", "solve", "ToptError", "ADVECTION", "CONTINUITY", "INCOMPRESSIBLE", "SCALARS"]
+
+ADVECTION, CONTINUITY, INCOMPRESSIBLE = 0, 1, 2
+MODELS = {"advection": 0, "continuity": 1, "incompressible": 2}
+SCALARS = {"obj": _lib.S_OBJ, "dist": _lib.S_DIST, "reg": _lib.S_REG, "grad_inf": _lib.S_GRAD_INF,
+           "gs": _lib.S_GS, "slv": _lib.S_SLV, "sls": _lib.S_SLS}
+EXIT = {0: "converged", 1: "iter_cap", 2: "stagnated"}
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _f32(t, device):
+    if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+        t = t.to(device=device, dtype=torch.float32).contiguous()
+    return t
+
+
+@dataclass
+class Config:
+    n: tuple               # paper order (n_1, ..., n_d)
+    nt: int
+    model: int = ADVECTION
+    reg_order: int = 2
+    alpha: float = 1e-2
+    window: int = 5
+    sigma: int = 1
+    tau: int = 0
+    method: int = 0        # 0 GA-NGMRES, 1 GA-AA
+    ordering: int = 0      # 0 Alg. 3, 1 reverse (aNGMRES[sigma]-FP[tau])
+    max_iter: int = 200
+    eps_rel: float = 5e-2
+    armijo_c: float = 1e-4
+    max_backtracks: int = 50
+
+    def params(self) -> Params:
+        p = Params()
+        d = len(self.n)
+        p.dim = d
+        nn = list(self.n) + [1] * (3 - d)
+        for i in range(3):
+            p.n[i] = int(nn[i])
+        p.nt, p.model, p.reg_order, p.alpha = self.nt, self.model, self.reg_order, self.alpha
+        p.window, p.sigma, p.tau = self.window, self.sigma, self.tau
+        p.method, p.ordering, p.max_iter = self.method, self.ordering, self.max_iter
+        p.eps_rel, p.armijo_c, p.max_backtracks = self.eps_rel, self.armijo_c, self.max_backtracks
+        return p
+
+
+class Topt:
+    """One problem context bound to a CUDA device and a torch-allocated workspace."""
+
+    def __init__(self, cfg: Config, device=None, rank: int = 0, world: int = 1, unique_id: bytes | None = None):
+        if not torch.cuda.is_available():
+            raise ToptError("a CUDA device is required (libtopt has no CPU path)")
+        self.cfg = cfg
+        self.device = torch.device(device if device is not None else f"cuda:{torch.cuda.current_device()}")
+        self.d = len(cfg.n)
+        self.shape = tuple(reversed(cfg.n))
+        self._p = cfg.params()
+        ctx = ctypes.c_void_p()
+        uid = ctypes.create_string_buffer(unique_id, 128) if unique_id else None
+        with torch.cuda.device(self.device):
+            check(LIB.topt_create(ctypes.byref(self._p), rank, world, uid, self.device.index,
+                                  ctypes.byref(ctx)), "topt_create")
+        self.ctx = ctx
+        nbytes = ctypes.c_size_t()
+        check(LIB.topt_workspace_size(self.ctx, ctypes.byref(nbytes)), "topt_workspace_size")
+        self.workspace = torch.empty(nbytes.value + 256, dtype=torch.uint8, device=self.device)
+        base = self.workspace.data_ptr()
+        off = (-base) % 256
+        check(LIB.topt_bind_workspace(self.ctx, ctypes.c_void_p(base + off), nbytes.value),
+              "topt_bind_workspace")
+        self.scalars = torch.zeros(_lib.NSCALARS, dtype=torch.float64, device=self.device)
+
+    def __del__(self):
+        try:
+            if getattr(self, "ctx", None):
+                LIB.topt_destroy(self.ctx)
+                self.ctx = None
+        except Exception:
+            pass
+
+    # -- helpers
+    def _vec(self):
+        return torch.empty((self.d,) + self.shape, dtype=torch.float32, device=self.device)
+
+    def _fld(self, k=1):
+        return torch.empty(((k,) if k > 1 else ()) + self.shape, dtype=torch.float32, device=self.device)
+
+    def scalars_dict(self, t=None):
+        t = self.scalars if t is None else t
+        h = t.cpu().tolist()
+        return {k: h[i] for k, i in SCALARS.items()}
+
+    # -- the benchmark unit
+    def eval_gradient(self, m0, m1, v, g=None, s=None, scalars=None):
+        m0, m1, v = (_f32(x, self.device) for x in (m0, m1, v))
+        g = self._vec() if g is None else g
+        s = self._vec() if s is None else s
+        sc = self.scalars if scalars is None else scalars
+        check(LIB.topt_eval_gradient(self.ctx, _ptr(m0), _ptr(m1), _ptr(v), _ptr(g), _ptr(s), _ptr(sc),
+                                     _stream()), "topt_eval_gradient")
+        return g, s, sc
+
+    def eval_gradient_host(self, m0_h, m1_h, v_h, g_h, scal_h):
+        """Host (pinned) buffers in, host buffers out; synchronous."""
+        check(LIB.topt_eval_gradient_host(self.ctx, _ptr(m0_h), _ptr(m1_h), _ptr(v_h), _ptr(g_h),
+                                          _ptr(scal_h), _stream()), "topt_eval_gradient_host")
+
+    def objective(self, m0, m1, v):
+        m0, m1, v = (_f32(x, self.device) for x in (m0, m1, v))
+        sc = torch.zeros(_lib.NSCALARS, dtype=torch.float64, device=self.device)
+        check(LIB.topt_objective(self.ctx, _ptr(m0), _ptr(m1), _ptr(v), _ptr(sc), _stream()), "topt_objective")
+        return self.scalars_dict(sc)
+
+    # -- operators
+    def feet(self, v):
+        v = _f32(v, self.device)
+        df, da = self._vec(), self._vec()
+        check(LIB.topt_feet(self.ctx, _ptr(v), _ptr(df), _ptr(da), _stream()), "topt_feet")
+        return df, da
+
+    def forward(self, m0, v):
+        m0, v = _f32(m0, self.device), _f32(v, self.device)
+        traj = self._fld(self.cfg.nt + 1)
+        check(LIB.topt_forward(self.ctx, _ptr(m0), _ptr(v), _ptr(traj), _stream()), "topt_forward")
+        return traj
+
+    def adjoint(self):
+        lam = self._fld(self.cfg.nt + 1)
+        b = self._vec()
+        check(LIB.topt_get_adjoint(self.ctx, _ptr(lam), _ptr(b), _stream()), "topt_get_adjoint")
+        return lam, b
+
+    def derivative(self, f, axis):
+        f = _f32(f, self.device)
+        out = self._fld()
+        check(LIB.topt_derivative(self.ctx, _ptr(f), axis, _ptr(out), _stream()), "topt_derivative")
+        return out
+
+    def apply_precond(self, g):
+        g = _f32(g, self.device)
+        s = self._vec()
+        check(LIB.topt_apply_precond(self.ctx, _ptr(g), _ptr(s), _stream()), "topt_apply_precond")
+        return s
+
+    def leray(self, u):
+        u = _f32(u, self.device)
+        out = self._vec()
+        check(LIB.topt_leray(self.ctx, _ptr(u), _ptr(out), _stream()), "topt_leray")
+        return out
+
+    def multidot(self, a, bs):
+        a = _f32(a, self.device)
+        bs = [_f32(b, self.device) for b in bs]
+        arr = (ctypes.c_void_p * len(bs))(*[b.data_ptr() for b in bs])
+        out = torch.zeros(len(bs), dtype=torch.float64, device=self.device)
+        check(LIB.topt_multidot(self.ctx, _ptr(a), arr, len(bs), _ptr(out), _stream()), "topt_multidot")
+        return out
+
+    def mix(self, q, vs, beta):
+        q = _f32(q, self.device)
+        vs = [_f32(x, self.device) for x in vs]
+        arr = (ctypes.c_void_p * max(1, len(vs)))(*[x.data_ptr() for x in vs])
+        b = (ctypes.c_double * max(1, len(beta)))(*[float(x) for x in beta])
+        out = self._vec()
+        check(LIB.topt_mix(self.ctx, _ptr(q), arr, b, len(vs), _ptr(out), _stream()), "topt_mix")
+        return out
+
+    # -- solver
+    def set_step_replay(self, rhos):
+        arr = (ctypes.c_double * max(1, len(rhos)))(*[float(r) for r in rhos])
+        check(LIB.topt_set_step_replay(self.ctx, arr, len(rhos)), "topt_set_step_replay")
+
+    def solve(self, m0, m1, v0=None):
+        m0, m1 = _f32(m0, self.device), _f32(m1, self.device)
+        v = torch.zeros((self.d,) + self.shape, dtype=torch.float32, device=self.device) if v0 is None \
+            else _f32(v0, self.device).clone()
+        rep = Report()
+        check(LIB.topt_solve(self.ctx, _ptr(m0), _ptr(m1), _ptr(v), ctypes.byref(rep), _stream()), "topt_solve")
+        out = rep.as_dict()
+        out["exit_name"] = EXIT.get(rep.exit, rep.exit)
+        return v, out
+
+
+def solve(m0, m1, alpha, nt, model="advection", window=5, mixing_period=None, sigma=1, tau=0,
+          reg_order=2, max_iter=200, eps_rel=5e-2, method="ngmres", ordering="ga", device=None):
+    """GA-NGMRES(w; sigma, tau) from v^0 = 0 (Alg. 3).  ``mixing_period`` P maps to
+    (sigma, tau) = (1, P - 1) (reading R14).  Returns (v, report)."""
+    if mixing_period is not None:
+        sigma, tau = 1, int(mixing_period) - 1
+    m0t = torch.as_tensor(m0)
+    n = tuple(reversed(m0t.shape))
+    cfg = Config(n=n, nt=nt, model=MODELS.get(model, model), reg_order=reg_order, alpha=alpha,
+                 window=window, sigma=sigma, tau=tau, method=0 if method == "ngmres" else 1,
+                 ordering=0 if ordering == "ga" else 1, max_iter=max_iter, eps_rel=eps_rel)
+    t = Topt(cfg, device=device)
+    return t.solve(m0t, torch.as_tensor(m1))

@@ -1,0 +1,187 @@
+// kernels_vec.cu — reductions, NGMRES Gram inner products and mixing (sm_100a).
+//
+// PAPER.md Alg. 1 line 5 / Alg. 3 line 8: the LSQ over
+// g(q) - g(v^{k-i}) is assembled on the host from fp64 inner products computed here
+// in one fused pass over a and every b_i ("multi-dot"); Alg. 1 line 6 / Alg. 3
+// line 9: v^{k+1} = q + sum beta_i (q - v^{k-i}) in one pass ("mix").
+// All reductions use fp64 per-block partials and a fixed-order finalisation.
+#include "internal.cuh"
+
+namespace topt {
+
+// dst = scale * (sum or max) of partials[slot * kMaxPartials + 0 .. nparts-1]
+__global__ void k_finalize(const double* __restrict__ partials, int nparts, double scale, int is_max,
+                           double* __restrict__ dst, size_t slot_stride) {
+  const double* p = partials + blockIdx.x * slot_stride;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) acc = is_max ? fmax(acc, p[i]) : acc + p[i];
+  __shared__ double sh[1024];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = is_max ? fmax(sh[threadIdx.x], sh[threadIdx.x + s])
+                                                  : sh[threadIdx.x] + sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) dst[blockIdx.x] = scale * sh[0];
+}
+
+void launch_finalize(const double* partials, int slot, int nparts, double scale, bool is_max,
+                     double* dst, cudaStream_t st) {
+  k_finalize<<<1, 1024, 0, st>>>(partials + (size_t)slot * kMaxPartials, nparts, scale, is_max ? 1 : 0,
+                                 dst, kMaxPartials);
+}
+
+void launch_finalize_multi(const double* partials, int slot0, int nslots, int nparts, double scale,
+                           double* dst, cudaStream_t st) {
+  k_finalize<<<nslots, 1024, 0, st>>>(partials + (size_t)slot0 * nparts, nparts, scale, 0, dst,
+                                      (size_t)nparts);
+}
+
+__global__ void k_combine_obj(double* s) { s[TOPT_S_OBJ] = s[TOPT_S_DIST] + s[TOPT_S_REG]; }
+void launch_combine_obj(double* scalars, cudaStream_t st) { k_combine_obj<<<1, 1, 0, st>>>(scalars); }
+
+// Multi-dot: partials[i * nblocks + block] = sum_x a(x) b_i(x), i in [i0, i0 + CH)
+template <int CH>
+__global__ void __launch_bounds__(kThreads) k_multidot(const float* __restrict__ a, VecList L, int i0,
+                                                       int count, size_t n4, double* __restrict__ partials) {
+  double acc[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) acc[c] = 0.0;
+  const float4* a4 = reinterpret_cast<const float4*>(a);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    const float4 x = a4[i];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      if (i0 + c < count) {
+        const float4 y = reinterpret_cast<const float4*>(L.p[i0 + c])[i];
+        acc[c] += (double)(x.x * y.x) + (double)(x.y * y.y) + (double)(x.z * y.z) + (double)(x.w * y.w);
+      }
+    }
+  }
+  __shared__ double sh[CH][kThreads / 32];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    double v = acc[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) sh[c][threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < CH && i0 + (int)threadIdx.x < count) {
+    double s = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) s += sh[threadIdx.x][w];
+    partials[(size_t)(i0 + threadIdx.x) * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+// Note: products are formed in fp32 (exact for fp32 x fp32 -> fp64 only if promoted first);
+// promote before multiplying so every product is exact in fp64.
+template <int CH>
+__global__ void __launch_bounds__(kThreads) k_multidot_exact(const float* __restrict__ a, VecList L, int i0,
+                                                             int count, size_t n4,
+                                                             double* __restrict__ partials) {
+  double acc[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) acc[c] = 0.0;
+  const float4* a4 = reinterpret_cast<const float4*>(a);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    const float4 x = a4[i];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      if (i0 + c < count) {
+        const float4 y = reinterpret_cast<const float4*>(L.p[i0 + c])[i];
+        double t = (double)x.x * (double)y.x;
+        t = fma((double)x.y, (double)y.y, t);
+        t = fma((double)x.z, (double)y.z, t);
+        t = fma((double)x.w, (double)y.w, t);
+        acc[c] += t;
+      }
+    }
+  }
+  __shared__ double sh[CH][kThreads / 32];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    double v = acc[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) sh[c][threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < CH && i0 + (int)threadIdx.x < count) {
+    double s = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) s += sh[threadIdx.x][w];
+    partials[(size_t)(i0 + threadIdx.x) * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+void launch_multidot(const float* a, const float* const* bs, int count, size_t n, double* partials,
+                     int* nparts, cudaStream_t st) {
+  VecList L;
+  for (int i = 0; i < count && i < kMaxVecs; ++i) L.p[i] = bs[i];
+  const size_t n4 = n / 4;
+  const int nb = grid_for(n4, kThreads, 148 * 8);
+  *nparts = nb;
+  constexpr int CH = 8;
+  for (int i0 = 0; i0 < count; i0 += CH)
+    k_multidot_exact<CH><<<nb, kThreads, 0, st>>>(a, L, i0, count, n4, partials);
+}
+
+// out = c0 q + sum_i c_i v_i  with c0 = 1 + sum beta, c_i = -beta_i
+__global__ void __launch_bounds__(kThreads) k_mix(const float* __restrict__ q, VecList L, float c0,
+                                                  int count, size_t n4, float* __restrict__ out) {
+  const float4* q4 = reinterpret_cast<const float4*>(q);
+  float4* o4 = reinterpret_cast<float4*>(out);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    const float4 x = q4[i];
+    float4 r = make_float4(c0 * x.x, c0 * x.y, c0 * x.z, c0 * x.w);
+    for (int c = 0; c < count; ++c) {
+      const float4 y = reinterpret_cast<const float4*>(L.p[c])[i];
+      const float cc = L.c[c];
+      r.x = fmaf(cc, y.x, r.x); r.y = fmaf(cc, y.y, r.y); r.z = fmaf(cc, y.z, r.z); r.w = fmaf(cc, y.w, r.w);
+    }
+    o4[i] = r;
+  }
+}
+
+void launch_mix(const float* q, const float* const* vs, const double* beta, int count, size_t n,
+                float* out, cudaStream_t st) {
+  VecList L;
+  double sb = 0.0;
+  for (int i = 0; i < count && i < kMaxVecs; ++i) {
+    L.p[i] = vs[i];
+    L.c[i] = (float)(-beta[i]);
+    sb += beta[i];
+  }
+  const size_t n4 = n / 4;
+  k_mix<<<grid_for(n4, kThreads, 148 * 8), kThreads, 0, st>>>(q, L, (float)(1.0 + sb), count, n4, out);
+}
+
+__global__ void k_axpy(const float* __restrict__ x, float a, const float* __restrict__ y, size_t n4,
+                       float* __restrict__ out) {
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  const float4* y4 = reinterpret_cast<const float4*>(y);
+  float4* o4 = reinterpret_cast<float4*>(out);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    const float4 u = x4[i], w = y4[i];
+    o4[i] = make_float4(fmaf(a, w.x, u.x), fmaf(a, w.y, u.y), fmaf(a, w.z, u.z), fmaf(a, w.w, u.w));
+  }
+}
+void launch_axpy(const float* x, float a, const float* y, size_t n, float* out, cudaStream_t st) {
+  k_axpy<<<grid_for(n / 4, kThreads, 148 * 8), kThreads, 0, st>>>(x, a, y, n / 4, out);
+}
+
+__global__ void k_sub(const float* __restrict__ a, const float* __restrict__ b, size_t n4, float* __restrict__ out) {
+  const float4* a4 = reinterpret_cast<const float4*>(a);
+  const float4* b4 = reinterpret_cast<const float4*>(b);
+  float4* o4 = reinterpret_cast<float4*>(out);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    const float4 u = a4[i], w = b4[i];
+    o4[i] = make_float4(u.x - w.x, u.y - w.y, u.z - w.z, u.w - w.w);
+  }
+}
+void launch_sub(const float* a, const float* b, size_t n, float* out, cudaStream_t st) {
+  k_sub<<<grid_for(n / 4, kThreads, 148 * 8), kThreads, 0, st>>>(a, b, n / 4, out);
+}
+
+}  // namespace topt

@@ -1,0 +1,112 @@
+"""GPU (sm_100a) vs fp64 oracle, per operator, through the C ABI.
+
+Tolerance (BASELINE.json north_star): relative L2 <= 1e-5 per operator on the same
+seeded inputs (inputs rounded to fp32 once and handed to both sides).
+"""
+import numpy as np
+import pytest
+
+from gpu_common import case, dev, host, rel_l2, topt_for
+from oracle import gradient as ogr
+from oracle import spectral, transport
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+GRIDS = [
+    (1, (64, 64)),          # 2D, config-1 recipe
+    (2, (32, 32, 32)),      # 3D cube, several tiles
+    (2, (64, 16, 8)),       # anisotropic, small last axis
+    (5, (16, 32, 64)),      # anisotropic, long last axis
+]
+
+
+@pytest.mark.parametrize("cfg,n", GRIDS)
+def test_feet(cfg, n):
+    d = case(cfg, n)
+    t = topt_for(d)
+    df, da = t.feet(dev(d["v"]))
+    rf, ra = transport.feet(d["grid"], d["v"], d["nt"])
+    assert rel_l2(host(df), rf) < TOL
+    assert rel_l2(host(da), ra) < TOL
+
+
+@pytest.mark.parametrize("cfg,n", GRIDS)
+@pytest.mark.parametrize("model", [0, 1])
+def test_forward_trajectory(cfg, n, model):
+    d = case(cfg, n, model=model)
+    t = topt_for(d)
+    traj = host(t.forward(dev(d["m0"]), dev(d["v"])))
+    _, _, _, ref = ogr.forward_solve(d["prob"], d["v"])
+    for j in range(d["nt"] + 1):
+        assert rel_l2(traj[j], ref[j]) < TOL, j
+
+
+def test_zero_velocity_identity_bitwise():
+    d = case(2, (32, 32, 32))
+    t = topt_for(d)
+    traj = host(t.forward(dev(d["m0"]), dev(np.zeros_like(d["v"]))))
+    for j in range(d["nt"] + 1):
+        assert np.array_equal(traj[j], d["m0"])
+
+
+@pytest.mark.parametrize("cfg,n", GRIDS)
+def test_derivatives(cfg, n):
+    d = case(cfg, n)
+    t = topt_for(d)
+    f = d["m0"]
+    for a in range(len(n)):
+        out = host(t.derivative(dev(f), a))
+        assert rel_l2(out, spectral.deriv(d["grid"], f, a)) < TOL, a
+
+
+@pytest.mark.parametrize("cfg,n", GRIDS)
+@pytest.mark.parametrize("model", [0, 2])
+def test_precond_and_leray(cfg, n, model):
+    d = case(cfg, n, model=model)
+    t = topt_for(d)
+    rng = np.random.default_rng(0)
+    g = np.stack([spectral.gaussian_blur(d["grid"], rng.normal(size=d["grid"].shape), 2.0)
+                  for _ in range(len(n))]).astype(np.float32).astype(np.float64)
+    s = host(t.apply_precond(dev(g)))
+    gg = spectral.leray(d["grid"], g) if model == 2 else g
+    ref = -spectral.apply_inv_alpha_L(d["grid"], gg, d["alpha"], d["reg_order"])
+    assert rel_l2(s, ref) < TOL
+    pl = host(t.leray(dev(g)))
+    assert rel_l2(pl, spectral.leray(d["grid"], g)) < TOL
+
+
+@pytest.mark.parametrize("cfg,n", GRIDS)
+@pytest.mark.parametrize("model", [0, 1, 2])
+def test_eval_gradient(cfg, n, model):
+    d = case(cfg, n, model=model)
+    if model == 2:
+        d["v"] = spectral.leray(d["grid"], d["v"]).astype(np.float32).astype(np.float64)
+    t = topt_for(d)
+    g, s, sc = t.eval_gradient(dev(d["m0"]), dev(d["m1"]), dev(d["v"]))
+    ref = ogr.evaluate(d["prob"], d["v"])
+    lam, b = t.adjoint()
+    lam, b = host(lam), host(b)
+    for j in range(d["nt"] + 1):
+        assert rel_l2(lam[j], ref["lam"][j]) < TOL, ("lam", j)
+    assert rel_l2(b, ref["b"]) < TOL, "b"
+    assert rel_l2(host(g), ref["g"]) < TOL, "g"
+    assert rel_l2(host(s), ref["s"]) < TOL, "s"
+    sd = t.scalars_dict(sc)
+    for k in ("obj", "dist", "reg", "grad_inf", "gs"):
+        assert abs(sd[k] - ref[k]) <= TOL * abs(ref[k]) + 1e-30, k
+
+
+def test_multidot_and_mix():
+    d = case(2, (32, 32, 32))
+    t = topt_for(d)
+    rng = np.random.default_rng(1)
+    a = rng.normal(size=d["v"].shape).astype(np.float32)
+    bs = [rng.normal(size=d["v"].shape).astype(np.float32) for _ in range(11)]
+    dots = t.multidot(dev(a), [dev(b) for b in bs]).cpu().numpy()
+    ref = [float(np.sum(a.astype(np.float64) * b.astype(np.float64))) for b in bs]
+    np.testing.assert_allclose(dots, ref, rtol=1e-12, atol=1e-9)
+    beta = rng.normal(size=11)
+    out = host(t.mix(dev(a), [dev(b) for b in bs], beta))
+    refm = (1 + beta.sum()) * a.astype(np.float64) - sum(bi * b.astype(np.float64) for bi, b in zip(beta, bs))
+    assert rel_l2(out, refm) < TOL
