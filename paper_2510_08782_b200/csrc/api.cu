@@ -62,13 +62,15 @@ struct topt_ctx {
   // workspace
   char* ws = nullptr;
   size_t ws_bytes = 0, ws_need = 0;
-  float *m_traj{}, *lam_traj{}, *df{}, *da{}, *E{}, *divv{}, *b{}, *tmp{};
-  float2* Z{};
+  float *m_traj{}, *lam_traj{}, *df{}, *da{}, *E{}, *divv{}, *b{}, *utmp{};
+  float2* Z{};      // b-chain: 3 complex fields of F
+  double2* Zv{};    // v-chain: 2 double-complex fields of F
   float *m0b{}, *m1b{}, *vb{}, *vt{};
   float *vcur{}, *gcur{}, *scur{}, *q{}, *gq{}, *sq{}, *vnew{}, *gnew{}, *snew{};
-  float* hist{};  // (w+1) slots x 2 vectors (NGMRES: v, g; AA: r, q)
+  float *ucur{}, *uq{}, *unew{};  // u = alpha L v tracked alongside v
+  float* hist{};  // (w+1) slots x 3 vectors (NGMRES: v, g, u; AA: r, q, u(q))
   double* partials{};
-  double* sc{};    // 4 sets of TOPT_NSCALARS: [0] current, [1] trial, [2] q, [3] new
+  double* sc{};    // 5 sets of 32: [0..15] public, [16..31] internal; sets: current, trial, q, new, scratch
   double* dots{};  // kMaxVecs doubles
   bool have_eval = false;
   std::vector<double> replay;
@@ -175,13 +177,14 @@ topt_status topt_create(const topt_params* p, int32_t rank, int32_t world, const
   add(V * 4); add(V * 4); // df, da
   add(F * 4); add(F * 4); // E, divv
   add(V * 4);             // b
-  add(F * 4);             // tmp
-  add(V * 8);             // Z (complex)
+  add(V * 4);             // utmp
+  add(3 * F * 8);         // Z (3 complex fields)
+  add(2 * F * 16);        // Zv (2 double-complex fields)
   add(F * 4); add(F * 4); add(V * 4); add(V * 4);  // m0b, m1b, vb, vt
-  for (int i = 0; i < 9; ++i) add(V * 4);          // vcur..snew
-  add(2 * W1 * V * 4);    // history
+  for (int i = 0; i < 12; ++i) add(V * 4);         // vcur..snew, ucur, uq, unew
+  add(3 * W1 * V * 4);    // history
   add((size_t)kNumSlots * kMaxPartials * 8);
-  add(4 * TOPT_NSCALARS * 8);
+  add(5 * 32 * 8);
   add(kMaxVecs * kMaxVecs * 8);
   c->ws_need = b;
   upload_twiddles();
@@ -225,17 +228,19 @@ topt_status topt_bind_workspace(topt_ctx* c, void* dptr, size_t bytes) {
   c->E = (float*)take(F * 4);
   c->divv = (float*)take(F * 4);
   c->b = (float*)take(V * 4);
-  c->tmp = (float*)take(F * 4);
-  c->Z = (float2*)take(V * 8);
+  c->utmp = (float*)take(V * 4);
+  c->Z = (float2*)take(3 * F * 8);
+  c->Zv = (double2*)take(2 * F * 16);
   c->m0b = (float*)take(F * 4);
   c->m1b = (float*)take(F * 4);
   c->vb = (float*)take(V * 4);
   c->vt = (float*)take(V * 4);
-  float** vecs[9] = {&c->vcur, &c->gcur, &c->scur, &c->q, &c->gq, &c->sq, &c->vnew, &c->gnew, &c->snew};
+  float** vecs[12] = {&c->vcur, &c->gcur, &c->scur, &c->q,    &c->gq,   &c->sq,
+                      &c->vnew, &c->gnew, &c->snew, &c->ucur, &c->uq,   &c->unew};
   for (auto pp : vecs) *pp = (float*)take(V * 4);
-  c->hist = (float*)take(2 * W1 * V * 4);
+  c->hist = (float*)take(3 * W1 * V * 4);
   c->partials = (double*)take((size_t)kNumSlots * kMaxPartials * 8);
-  c->sc = (double*)take(4 * TOPT_NSCALARS * 8);
+  c->sc = (double*)take(5 * 32 * 8);
   c->dots = (double*)take(kMaxVecs * kMaxVecs * 8);
   return TOPT_OK;
 }
@@ -254,6 +259,8 @@ topt_status topt_local_slab(const topt_ctx* ctx, int32_t* z0, int32_t* nz) {
 // ======================================================================================
 namespace {
 
+constexpr int kSet = 32;  // doubles per scalar set: [0, 16) public, [16, 32) internal
+
 topt_status need_ws(topt_ctx* c) {
   if (!c) return fail(TOPT_ERR_INVALID_ARG, "ctx is NULL");
   if (!c->ws) return fail(TOPT_ERR_WORKSPACE, "no workspace bound");
@@ -261,6 +268,9 @@ topt_status need_ws(topt_ctx* c) {
 }
 
 bool aligned16(const void* p) { return (((uintptr_t)p) & 15) == 0; }
+
+double* pub(topt_ctx* c, int set) { return c->sc + set * kSet; }
+double* intl(topt_ctx* c, int set) { return c->sc + set * kSet + 16; }
 
 // div v = sum_a d_a v_a (R3), into c->divv
 void compute_div(topt_ctx* c, const float* v, cudaStream_t st) {
@@ -271,14 +281,16 @@ void compute_div(topt_ctx* c, const float* v, cudaStream_t st) {
   }
 }
 
-// Forward half: feet (forward, and adjoint if want_adj), static factor for the model,
-// trajectory m^0..m^S (m_traj), lam^S, dist -> scalars[DIST].
-void forward_half(topt_ctx* c, const float* m0, const float* m1, const float* v, bool want_adj,
-                  double* scal, cudaStream_t st) {
+// Forward half: feet (R6), static factor (continuity, R7), m^0..m^S in m_traj,
+// lam^S = m1 - m^S (R1/R8), dist -> scal[DIST], sum_x v_c -> isc[I_SUMV..].
+void forward_half(topt_ctx* c, const float* m0, const float* m1, const float* v, bool want_adj, double* scal,
+                  double* isc, cudaStream_t st) {
   const Geom& g = c->g;
   const int S = c->p.nt;
   const size_t F = c->F;
-  launch_trace(g, v, c->df, want_adj ? c->da : nullptr, st);
+  int np = 0;
+  launch_trace(g, v, c->df, want_adj ? c->da : nullptr, c->partials, &np, st);
+  launch_finalize_slots(c->partials, 0, c->d, np, false, isc + I_SUMV, st);
   const float* Ef = nullptr;
   if (c->p.model == TOPT_CONTINUITY) {
     compute_div(c, v, st);
@@ -286,58 +298,61 @@ void forward_half(topt_ctx* c, const float* m0, const float* m1, const float* v,
     Ef = c->E;
   }
   cudaMemcpyAsync(c->m_traj, m0, F * 4, cudaMemcpyDeviceToDevice, st);
-  for (int j = 0; j + 1 < S; ++j)
-    launch_sl_step(g, c->m_traj + j * F, c->df, Ef, c->m_traj + (j + 1) * F, st);
-  int np = 0;
-  launch_sl_last(g, c->m_traj + (S - 1) * F, c->df, Ef, m1, c->m_traj + S * F, c->lam_traj + S * F,
-                 c->partials, &np, st);
+  for (int j = 0; j + 1 < S; ++j) launch_sl_step(g, c->m_traj + j * F, c->df, Ef, c->m_traj + (j + 1) * F, st);
+  launch_sl_last(g, c->m_traj + (S - 1) * F, c->df, Ef, m1, c->m_traj + S * F, c->lam_traj + S * F, c->partials,
+                 &np, st);
   launch_finalize(c->partials, 0, np, 0.5 * c->cellvol, false, scal + TOPT_S_DIST, st);
 }
 
-// Adjoint half + body force + preconditioner.  Requires forward_half(want_adj=true) or
-// (want_adj=false followed by an adjoint trace, done here when need_trace).
-void backward_half(topt_ctx* c, const float* v, float* gout, float* sout, double* scal, bool need_trace,
-                   cudaStream_t st) {
+// Backward half: adjoint sweep (advection: Heun factor, R7), body force (2.2)/(R8) with
+// trapezoid weights (R10), then g = alpha L v + b (P_L b for incompressible, R9) and
+// s = -(alpha L~)^{-1} g = -P_0 v - (alpha L~)^{-1} b.  alpha L v is `u` when the
+// caller tracks it (solver), otherwise computed by the fp64 v-chain.
+void backward_half(topt_ctx* c, const float* v, const float* u, float* gout, float* sout, double* scal,
+                   double* isc, cudaStream_t st) {
   const Geom& g = c->g;
   const int S = c->p.nt;
   const size_t F = c->F;
-  if (need_trace) launch_trace(g, v, nullptr, c->da, st);
   const float* Ea = nullptr;
   if (c->p.model == TOPT_ADVECTION) {
     compute_div(c, v, st);
     launch_efactor(g, c->divv, c->da, (float)(0.5 * c->dt), (float)(0.5 * c->dt * c->dt), c->E, st);
     Ea = c->E;
   }
-  for (int j = S - 1; j >= 0; --j)
-    launch_sl_step(g, c->lam_traj + (j + 1) * F, c->da, Ea, c->lam_traj + j * F, st);
-  // body force (2.2) / (R8), trapezoid weights (R10)
+  for (int j = S - 1; j >= 0; --j) launch_sl_step(g, c->lam_traj + (j + 1) * F, c->da, Ea, c->lam_traj + j * F, st);
   std::vector<double> w = c->wts;
   const bool cont = c->p.model == TOPT_CONTINUITY;
   if (cont)
     for (auto& x : w) x = -x;
   for (int a = 0; a < c->d; ++a) {
-    DerivArgs da{cont ? c->lam_traj : c->m_traj, F, cont ? c->m_traj : c->lam_traj, F, w.data(), S + 1,
-                 0.f, c->b + a * F};
+    DerivArgs da{cont ? c->lam_traj : c->m_traj, F, cont ? c->m_traj : c->lam_traj, F, w.data(), S + 1, 0.f,
+                 c->b + a * F};
     launch_deriv_accum(g, a, da, st);
   }
-  PrecondArgs pa{v, c->b, c->Z, gout, sout, c->p.alpha, c->p.reg_order,
-                 c->p.model == TOPT_INCOMPRESSIBLE, c->partials, scal, c->cellvol};
-  launch_precond(g, pa, st);
-  launch_combine_obj(scal, st);
+  if (!u) {
+    launch_vchain(g, v, c->Zv, c->utmp, c->p.alpha, c->p.reg_order, st);
+    u = c->utmp;
+  }
+  const bool leray = c->p.model == TOPT_INCOMPRESSIBLE;
+  launch_bchain(g, c->b, c->Z, c->p.alpha, c->p.reg_order, leray, st);
+  int np = 0;
+  launch_assemble(g, c->Z, leray, c->b, u, v, isc + I_SUMV, gout, sout, c->partials, &np, st);
+  launch_finalize_slots(c->partials, 0, 10, np, true, isc + I_GMAX, st);
+  launch_finish(isc, scal, c->d, (double)F, c->cellvol, st);
 }
 
-topt_status eval_gradient(topt_ctx* c, const float* m0, const float* m1, const float* v, float* gout,
-                          float* sout, double* scal, cudaStream_t st) {
-  forward_half(c, m0, m1, v, true, scal, st);
-  backward_half(c, v, gout, sout, scal, false, st);
+topt_status eval_gradient(topt_ctx* c, const float* m0, const float* m1, const float* v, const float* u,
+                          float* gout, float* sout, double* scal, double* isc, cudaStream_t st) {
+  forward_half(c, m0, m1, v, true, scal, isc, st);
+  backward_half(c, v, u, gout, sout, scal, isc, st);
   TOPT_CHECK_LAUNCH();
   return TOPT_OK;
 }
 
-// Forward-only trial objective: dist (device scalar); trajectory left in m_traj.
-topt_status trial_dist(topt_ctx* c, const float* m0, const float* m1, const float* v, double* scal,
+// Forward-only trial objective (the Armijo trial): scal[DIST].
+topt_status trial_dist(topt_ctx* c, const float* m0, const float* m1, const float* v, double* scal, double* isc,
                        cudaStream_t st) {
-  forward_half(c, m0, m1, v, false, scal, st);
+  forward_half(c, m0, m1, v, false, scal, isc, st);
   TOPT_CHECK_LAUNCH();
   return TOPT_OK;
 }
@@ -354,7 +369,7 @@ void jacobi_eigen(int n, std::vector<double>& A, std::vector<double>& V, std::ve
         tot += A[i * n + j] * A[i * n + j];
         if (i != j) off += A[i * n + j] * A[i * n + j];
       }
-    if (off <= 1e-30 * tot || off == 0.0) break;
+    if (off == 0.0 || off <= 1e-30 * tot) break;
     for (int p = 0; p < n - 1; ++p)
       for (int q = p + 1; q < n; ++q) {
         const double apq = A[p * n + q];
@@ -384,8 +399,8 @@ void jacobi_eigen(int n, std::vector<double>& A, std::vector<double>& V, std::ve
   for (int i = 0; i < n; ++i) ev[i] = A[i * n + i];
 }
 
-// argmin_beta || r + C beta ||: G = C^T C (n x n), rhs = C^T r.  Minimum-norm solution with
-// eigenvalues below 1e-12 lambda_max dropped (R15: singular values below 1e-6 sigma_max).
+// argmin_beta || r + C beta ||_2 from G = C^T C and rhs = C^T r: minimum-norm solution with
+// eigenvalues of G below 1e-12 lambda_max dropped (R15: singular values of C below 1e-6 sigma_max).
 std::vector<double> lsq_from_gram(int n, const std::vector<double>& G, const std::vector<double>& rhs) {
   std::vector<double> A = G, V, ev;
   jacobi_eigen(n, A, V, ev);
@@ -404,18 +419,20 @@ std::vector<double> lsq_from_gram(int n, const std::vector<double>& G, const std
 }
 
 struct HostScalars {
-  double v[TOPT_NSCALARS];
+  double v[kSet];
+  double pub(int i) const { return v[i]; }
+  double in(int i) const { return v[16 + i]; }
 };
 
 topt_status fetch(topt_ctx* c, int set, HostScalars& out, cudaStream_t st) {
-  TOPT_CUDA(cudaMemcpyAsync(out.v, c->sc + set * TOPT_NSCALARS, sizeof(out.v), cudaMemcpyDeviceToHost, st));
+  TOPT_CUDA(cudaMemcpyAsync(out.v, c->sc + set * kSet, sizeof(out.v), cudaMemcpyDeviceToHost, st));
   TOPT_CUDA(cudaStreamSynchronize(st));
   return TOPT_OK;
 }
 
 // dots[i] = <a, bs[i]> (unweighted l2 over d*F entries), returned on the host
-topt_status host_dots(topt_ctx* c, const float* a, const std::vector<const float*>& bs,
-                      std::vector<double>& out, cudaStream_t st) {
+topt_status host_dots(topt_ctx* c, const float* a, const std::vector<const float*>& bs, std::vector<double>& out,
+                      cudaStream_t st) {
   out.assign(bs.size(), 0.0);
   if (bs.empty()) return TOPT_OK;
   int np = 0;
@@ -425,6 +442,13 @@ topt_status host_dots(topt_ctx* c, const float* a, const std::vector<const float
   TOPT_CUDA(cudaMemcpyAsync(out.data(), c->dots, bs.size() * 8, cudaMemcpyDeviceToHost, st));
   TOPT_CUDA(cudaStreamSynchronize(st));
   return TOPT_OK;
+}
+
+// in-place Leray projection of a vector field (b-chain with b := x, assemble writes P_L x)
+void leray_inplace(topt_ctx* c, float* x, cudaStream_t st) {
+  launch_bchain(c->g, x, c->Z, c->p.alpha, c->p.reg_order, true, st);
+  int np = 0;
+  launch_assemble(c->g, c->Z, true, nullptr, nullptr, nullptr, nullptr, x, nullptr, c->partials, &np, st);
 }
 
 double now() {
@@ -438,19 +462,18 @@ double now() {
 // ======================================================================================
 extern "C" {
 
-topt_status topt_eval_gradient(topt_ctx* c, const float* m0, const float* m1, const float* v, float* g,
-                               float* s, double* d_scalars, void* stream) {
+topt_status topt_eval_gradient(topt_ctx* c, const float* m0, const float* m1, const float* v, float* g, float* s,
+                               double* d_scalars, void* stream) {
   topt_status s0 = need_ws(c);
   if (s0 != TOPT_OK) return s0;
   if (!m0 || !m1 || !v || !d_scalars) return fail(TOPT_ERR_INVALID_ARG, "NULL argument");
   if (!aligned16(m0) || !aligned16(m1) || !aligned16(v) || (g && !aligned16(g)) || (s && !aligned16(s)))
     return fail(TOPT_ERR_INVALID_ARG, "pointers must be 16-byte aligned");
-  cudaStream_t st = (cudaStream_t)stream;
-  return eval_gradient(c, m0, m1, v, g, s, d_scalars, st);
+  return eval_gradient(c, m0, m1, v, nullptr, g, s, d_scalars, intl(c, 4), (cudaStream_t)stream);
 }
 
-topt_status topt_eval_gradient_host(topt_ctx* c, const float* m0_h, const float* m1_h, const float* v_h,
-                                    float* g_h, double* h_scalars, void* stream) {
+topt_status topt_eval_gradient_host(topt_ctx* c, const float* m0_h, const float* m1_h, const float* v_h, float* g_h,
+                                    double* h_scalars, void* stream) {
   topt_status s0 = need_ws(c);
   if (s0 != TOPT_OK) return s0;
   if (!m0_h || !m1_h || !v_h || !h_scalars) return fail(TOPT_ERR_INVALID_ARG, "NULL argument");
@@ -458,10 +481,10 @@ topt_status topt_eval_gradient_host(topt_ctx* c, const float* m0_h, const float*
   TOPT_CUDA(cudaMemcpyAsync(c->m0b, m0_h, c->F * 4, cudaMemcpyHostToDevice, st));
   TOPT_CUDA(cudaMemcpyAsync(c->m1b, m1_h, c->F * 4, cudaMemcpyHostToDevice, st));
   TOPT_CUDA(cudaMemcpyAsync(c->vb, v_h, c->vecN * 4, cudaMemcpyHostToDevice, st));
-  topt_status r = eval_gradient(c, c->m0b, c->m1b, c->vb, c->gcur, c->scur, c->sc, st);
+  topt_status r = eval_gradient(c, c->m0b, c->m1b, c->vb, nullptr, c->gcur, c->scur, pub(c, 4), intl(c, 4), st);
   if (r != TOPT_OK) return r;
   if (g_h) TOPT_CUDA(cudaMemcpyAsync(g_h, c->gcur, c->vecN * 4, cudaMemcpyDeviceToHost, st));
-  TOPT_CUDA(cudaMemcpyAsync(h_scalars, c->sc, TOPT_NSCALARS * 8, cudaMemcpyDeviceToHost, st));
+  TOPT_CUDA(cudaMemcpyAsync(h_scalars, pub(c, 4), TOPT_NSCALARS * 8, cudaMemcpyDeviceToHost, st));
   TOPT_CUDA(cudaStreamSynchronize(st));
   return TOPT_OK;
 }
@@ -472,12 +495,13 @@ topt_status topt_objective(topt_ctx* c, const float* m0, const float* m1, const 
   if (s0 != TOPT_OK) return s0;
   if (!m0 || !m1 || !v || !d_scalars) return fail(TOPT_ERR_INVALID_ARG, "NULL argument");
   cudaStream_t st = (cudaStream_t)stream;
-  forward_half(c, m0, m1, v, false, d_scalars, st);
-  PrecondArgs pa{v, nullptr, c->Z, nullptr, nullptr, c->p.alpha, c->p.reg_order, false, c->partials,
-                 c->sc + 3 * TOPT_NSCALARS, c->cellvol};
-  launch_precond(c->g, pa, st);
-  TOPT_CUDA(cudaMemcpyAsync(d_scalars + TOPT_S_REG, c->sc + 3 * TOPT_NSCALARS + TOPT_S_REG, 8,
-                            cudaMemcpyDeviceToDevice, st));
+  forward_half(c, m0, m1, v, false, d_scalars, intl(c, 4), st);
+  // reg = alpha/2 <v, L v>_h = h^d/2 sum v u,  u = alpha L v (fp64 chain)
+  launch_vchain(c->g, v, c->Zv, c->utmp, c->p.alpha, c->p.reg_order, st);
+  const float* bs[1] = {c->utmp};
+  int np = 0;
+  launch_multidot(v, bs, 1, c->vecN, c->partials, &np, st);
+  launch_finalize_multi(c->partials, 0, 1, np, 0.5 * c->cellvol, d_scalars + TOPT_S_REG, st);
   launch_combine_obj(d_scalars, st);
   TOPT_CHECK_LAUNCH();
   return TOPT_OK;
@@ -487,7 +511,7 @@ topt_status topt_feet(topt_ctx* c, const float* v, float* delta_f, float* delta_
   topt_status s0 = need_ws(c);
   if (s0 != TOPT_OK) return s0;
   if (!v || (!delta_f && !delta_a)) return fail(TOPT_ERR_INVALID_ARG, "NULL argument");
-  launch_trace(c->g, v, delta_f, delta_a, (cudaStream_t)stream);
+  launch_trace(c->g, v, delta_f, delta_a, nullptr, nullptr, (cudaStream_t)stream);
   TOPT_CHECK_LAUNCH();
   return TOPT_OK;
 }
@@ -497,8 +521,7 @@ topt_status topt_forward(topt_ctx* c, const float* m0, const float* v, float* m_
   if (s0 != TOPT_OK) return s0;
   if (!m0 || !v || !m_traj) return fail(TOPT_ERR_INVALID_ARG, "NULL argument");
   cudaStream_t st = (cudaStream_t)stream;
-  // m1 unused for the trajectory; pass m0 so lam^S/dist are well defined scratch values
-  forward_half(c, m0, m0, v, false, c->sc + 3 * TOPT_NSCALARS, st);
+  forward_half(c, m0, m0, v, false, pub(c, 4), intl(c, 4), st);
   TOPT_CUDA(cudaMemcpyAsync(m_traj, c->m_traj, (c->p.nt + 1) * c->F * 4, cudaMemcpyDeviceToDevice, st));
   TOPT_CHECK_LAUNCH();
   return TOPT_OK;
@@ -530,9 +553,11 @@ topt_status topt_apply_precond(topt_ctx* c, const float* g, float* s, void* stre
   topt_status s0 = need_ws(c);
   if (s0 != TOPT_OK) return s0;
   if (!g || !s) return fail(TOPT_ERR_INVALID_ARG, "NULL argument");
-  PrecondArgs pa{nullptr, g, c->Z, nullptr, s, c->p.alpha, c->p.reg_order,
-                 c->p.model == TOPT_INCOMPRESSIBLE, c->partials, nullptr, c->cellvol};
-  launch_precond(c->g, pa, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool leray = c->p.model == TOPT_INCOMPRESSIBLE;
+  launch_bchain(c->g, g, c->Z, c->p.alpha, c->p.reg_order, leray, st);
+  int np = 0;
+  launch_assemble(c->g, c->Z, leray, g, nullptr, nullptr, nullptr, nullptr, s, c->partials, &np, st);
   TOPT_CHECK_LAUNCH();
   return TOPT_OK;
 }
@@ -541,9 +566,10 @@ topt_status topt_leray(topt_ctx* c, const float* u, float* out, void* stream) {
   topt_status s0 = need_ws(c);
   if (s0 != TOPT_OK) return s0;
   if (!u || !out) return fail(TOPT_ERR_INVALID_ARG, "NULL argument");
-  PrecondArgs pa{nullptr, u, c->Z, out, nullptr, c->p.alpha, c->p.reg_order, true, c->partials, nullptr,
-                 c->cellvol};
-  launch_precond(c->g, pa, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  launch_bchain(c->g, u, c->Z, c->p.alpha, c->p.reg_order, true, st);
+  int np = 0;
+  launch_assemble(c->g, c->Z, true, nullptr, nullptr, nullptr, nullptr, out, nullptr, c->partials, &np, st);
   TOPT_CHECK_LAUNCH();
   return TOPT_OK;
 }
@@ -578,7 +604,9 @@ topt_status topt_set_step_replay(topt_ctx* c, const double* rho, int32_t count) 
   return TOPT_OK;
 }
 
-// GA-NGMRES(w; sigma, tau) (Alg. 3) / GA-AA, host-driven.
+// GA-NGMRES(w; sigma, tau) (Alg. 3) / GA-AA, host-driven.  u = alpha L v is carried with
+// every iterate (q: u_q = u - rho P_0 g since alpha L s = -P_0 g; mixing is linear), so the
+// evaluations inside the solve never apply L to a stored fp32 field.
 topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_inout, topt_report* rep,
                        void* stream) {
   topt_status s0 = need_ws(c);
@@ -589,30 +617,22 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
   const size_t V = c->vecN;
   const int W1 = P.window + 1;
   const bool aa = P.method == TOPT_GA_AA;
+  const bool leray = P.model == TOPT_INCOMPRESSIBLE;
+  const double nF = (double)c->F;
   std::memset(rep, 0, sizeof(*rep));
   const double t0 = now();
   double t_pde = 0.0, t_ls = 0.0;
   int grad_evals = 0, obj_evals = 0, nsteps = 0;
   std::deque<double> replay(c->replay.begin(), c->replay.end());
+  topt_status r;
 
-  auto slot_a = [&](int i) { return c->hist + (size_t)(2 * i) * V; };      // NGMRES: v ; AA: r
-  auto slot_b = [&](int i) { return c->hist + (size_t)(2 * i + 1) * V; };  // NGMRES: g ; AA: q
-  std::deque<int> win;                       // ring slots, most recent last
-  std::vector<std::vector<double>> H(W1, std::vector<double>(W1, 0.0));  // <g_i, g_j> by slot
-
-  // v^0 and g(v^0)
-  TOPT_CUDA(cudaMemcpyAsync(c->vcur, v_inout, V * 4, cudaMemcpyDeviceToDevice, st));
-  double te = now();
-  topt_status r = eval_gradient(c, m0, m1, c->vcur, c->gcur, c->scur, c->sc, st);
-  if (r != TOPT_OK) return r;
-  ++grad_evals;
-  HostScalars cur;
-  if ((r = fetch(c, 0, cur, st)) != TOPT_OK) return r;
-  t_pde += now() - te;
-  const double g0 = cur.v[TOPT_S_GRAD_INF];
-  rep->grad_inf0 = g0;
-
-  auto push_ngmres = [&](const float* v, const float* g) -> topt_status {
+  // history slot i: A = v (AA: r), B = g (AA: q), U = u (AA: u(q))
+  auto slotA = [&](int i) { return c->hist + (size_t)(3 * i) * V; };
+  auto slotB = [&](int i) { return c->hist + (size_t)(3 * i + 1) * V; };
+  auto slotU = [&](int i) { return c->hist + (size_t)(3 * i + 2) * V; };
+  std::deque<int> win;  // ring slots, most recent last
+  std::vector<std::vector<double>> H(W1, std::vector<double>(W1, 0.0));  // <B_i, B_j> by slot
+  auto take_slot = [&]() {
     int slot;
     if ((int)win.size() < W1) {
       slot = (int)win.size();
@@ -620,32 +640,84 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
       slot = win.front();
       win.pop_front();
     }
-    TOPT_CUDA(cudaMemcpyAsync(slot_a(slot), v, V * 4, cudaMemcpyDeviceToDevice, st));
-    TOPT_CUDA(cudaMemcpyAsync(slot_b(slot), g, V * 4, cudaMemcpyDeviceToDevice, st));
+    return slot;
+  };
+  // push (a, b, u) and refresh the Gram row of b against the window
+  auto push = [&](const float* a, const float* b, const float* u, bool gram) -> topt_status {
+    const int slot = take_slot();
+    TOPT_CUDA(cudaMemcpyAsync(slotA(slot), a, V * 4, cudaMemcpyDeviceToDevice, st));
+    TOPT_CUDA(cudaMemcpyAsync(slotB(slot), b, V * 4, cudaMemcpyDeviceToDevice, st));
+    TOPT_CUDA(cudaMemcpyAsync(slotU(slot), u, V * 4, cudaMemcpyDeviceToDevice, st));
     win.push_back(slot);
+    if (!gram) return TOPT_OK;
     std::vector<const float*> bs;
-    for (int s2 : win) bs.push_back(slot_b(s2));
+    for (int s2 : win) bs.push_back(slotB(s2));
     std::vector<double> dd;
-    topt_status rr = host_dots(c, slot_b(slot), bs, dd, st);
+    topt_status rr = host_dots(c, slotB(slot), bs, dd, st);
     if (rr != TOPT_OK) return rr;
-    for (size_t i = 0; i < win.size(); ++i) {
-      H[slot][win[i]] = dd[i];
-      H[win[i]][slot] = dd[i];
-    }
+    for (size_t i = 0; i < win.size(); ++i) H[slot][win[i]] = H[win[i]][slot] = dd[i];
     return TOPT_OK;
   };
-  if (!aa) {
-    if ((r = push_ngmres(c->vcur, c->gcur)) != TOPT_OK) return r;
-  }
+
+  // v^0, u^0 = alpha L v^0 (fp64 chain, once), g(v^0)
+  TOPT_CUDA(cudaMemcpyAsync(c->vcur, v_inout, V * 4, cudaMemcpyDeviceToDevice, st));
+  if (leray) leray_inplace(c, c->vcur, st);
+  launch_vchain(c->g, c->vcur, c->Zv, c->ucur, P.alpha, P.reg_order, st);
+  double te = now();
+  if ((r = eval_gradient(c, m0, m1, c->vcur, c->ucur, c->gcur, c->scur, pub(c, 0), intl(c, 0), st)) != TOPT_OK)
+    return r;
+  ++grad_evals;
+  HostScalars cur, qs, ns;
+  if ((r = fetch(c, 0, cur, st)) != TOPT_OK) return r;
+  t_pde += now() - te;
+  const double g0 = cur.pub(TOPT_S_GRAD_INF);
+  rep->grad_inf0 = g0;
+  if (!aa && (r = push(c->vcur, c->gcur, c->ucur, true)) != TOPT_OK) return r;
+
+  // q-state helpers: v_q = v + rho s, u_q = u - rho (g - gbar)
+  auto make_q = [&](double rho_) {
+    launch_axpy(c->vcur, (float)rho_, c->scur, V, c->q, st);
+    float cst[3] = {0.f, 0.f, 0.f};
+    for (int a = 0; a < c->d; ++a) cst[a] = (float)(rho_ * cur.in(I_SUMG + a) / nF);
+    launch_axpy_c(c->ucur, (float)(-rho_), c->gcur, V, c->d, cst, c->uq, st);
+  };
+  auto eval_q = [&]() -> topt_status {
+    topt_status rr = eval_gradient(c, m0, m1, c->q, c->uq, c->gq, c->sq, pub(c, 2), intl(c, 2), st);
+    if (rr != TOPT_OK) return rr;
+    ++grad_evals;
+    return fetch(c, 2, qs, st);
+  };
+  auto accept_q = [&]() {
+    std::swap(c->vcur, c->q);
+    std::swap(c->ucur, c->uq);
+    std::swap(c->gcur, c->gq);
+    std::swap(c->scur, c->sq);
+    cur = qs;
+  };
+  auto eval_new = [&]() -> topt_status {
+    if (leray) {
+      leray_inplace(c, c->vnew, st);
+      leray_inplace(c, c->unew, st);
+    }
+    topt_status rr = eval_gradient(c, m0, m1, c->vnew, c->unew, c->gnew, c->snew, pub(c, 3), intl(c, 3), st);
+    if (rr != TOPT_OK) return rr;
+    ++grad_evals;
+    rr = fetch(c, 3, ns, st);
+    if (rr != TOPT_OK) return rr;
+    std::swap(c->vcur, c->vnew);
+    std::swap(c->ucur, c->unew);
+    std::swap(c->gcur, c->gnew);
+    std::swap(c->scur, c->snew);
+    cur = ns;
+    return TOPT_OK;
+  };
 
   double rho = 1.0;
   int k = 0;
   int exit_code = TOPT_ITER_CAP;
-  HostScalars qs, ns;
-  while (true) {
-    if (P.max_iter == 0) break;
-    // ---- q(v^k): Armijo backtracking with memory --------------------------
-    const double obj0 = cur.v[TOPT_S_OBJ], gs = cur.v[TOPT_S_GS];
+  while (P.max_iter > 0) {
+    // ---- q(v^k): Armijo backtracking with memory (R12) ---------------------
+    const double obj0 = cur.pub(TOPT_S_OBJ), gs = cur.pub(TOPT_S_GS);
     bool accepted = false;
     double rho_t = rho;
     te = now();
@@ -653,18 +725,19 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
       rho_t = replay.front();
       replay.pop_front();
       rho = rho_t;
-      launch_axpy(c->vcur, (float)rho_t, c->scur, V, c->q, st);
+      make_q(rho_t);
       accepted = true;
     } else {
       for (int t = 0; t <= P.max_backtracks; ++t) {
-        launch_axpy(c->vcur, (float)rho_t, c->scur, V, c->q, st);
-        if ((r = trial_dist(c, m0, m1, c->q, c->sc + 1 * TOPT_NSCALARS, st)) != TOPT_OK) return r;
+        make_q(rho_t);
+        if ((r = trial_dist(c, m0, m1, c->q, pub(c, 1), intl(c, 1), st)) != TOPT_OK) return r;
         ++obj_evals;
         HostScalars ts;
         if ((r = fetch(c, 1, ts, st)) != TOPT_OK) return r;
-        const double reg_t = cur.v[TOPT_S_REG] + rho_t * cur.v[TOPT_S_SLV] +
-                             0.5 * rho_t * rho_t * cur.v[TOPT_S_SLS];
-        const double obj_t = ts.v[TOPT_S_DIST] + reg_t;
+        // reg(v + rho s) = reg + rho alpha<s, L v> + rho^2/2 alpha<s, L s>  (exact: quadratic)
+        const double reg_t = cur.pub(TOPT_S_REG) + rho_t * cur.pub(TOPT_S_SLV) +
+                             0.5 * rho_t * rho_t * cur.pub(TOPT_S_SLS);
+        const double obj_t = ts.pub(TOPT_S_DIST) + reg_t;
         if (obj_t < obj0 + rho_t * P.armijo_c * gs) {
           accepted = true;
           rho = t == 0 ? 2.0 * rho_t : rho_t;
@@ -678,141 +751,97 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
       t_pde += now() - te;
       break;
     }
-    // g(q): needed by every NGMRES / FP step; AA needs it only when it takes the FP branch
-    auto eval_q = [&]() -> topt_status {
-      topt_status rr = eval_gradient(c, m0, m1, c->q, c->gq, c->sq, c->sc + 2 * TOPT_NSCALARS, st);
-      if (rr != TOPT_OK) return rr;
-      ++grad_evals;
-      return fetch(c, 2, qs, st);
-    };
-    if (!aa) {
-      if ((r = eval_q()) != TOPT_OK) return r;
-    }
     t_pde += now() - te;
 
     const int period = P.sigma + P.tau;
     const bool fp_step = P.ordering == TOPT_ORDER_GA ? (k % period >= P.sigma) : (k % period < P.tau);
     const int wk = std::min(k, P.window);
     if (!aa) {
+      te = now();
+      if ((r = eval_q()) != TOPT_OK) return r;  // g(q): both branches need it (R17)
+      t_pde += now() - te;
       if (fp_step) {
-        std::swap(c->vcur, c->q);
-        std::swap(c->gcur, c->gq);
-        std::swap(c->scur, c->sq);
-        cur = qs;
+        accept_q();
       } else {
-        // LSQ (Alg. 3 line 8): columns C_i = g_q - g(v^{k-i}), i = 0..w_k (R13)
+        // LSQ (Alg. 3 line 8): columns C_i = g_q - g(v^{k-i}), i = 0..w_k (R13), from the
+        // fp64 Gram: G_ij = <g_q,g_q> - <g_q,g_i> - <g_q,g_j> + <g_i,g_j>, rhs_i = <C_i, g_q>
         const double tl = now();
-        const int m = (int)win.size();  // == wk + 1
-        (void)wk;
+        const int m = (int)win.size();  // == w_k + 1
         std::vector<const float*> bs;
-        for (int i = 0; i < m; ++i) bs.push_back(slot_b(win[m - 1 - i]));  // i = 0 -> v^k
+        for (int i = 0; i < m; ++i) bs.push_back(slotB(win[m - 1 - i]));  // i = 0 -> v^k
         bs.push_back(c->gq);
-        std::vector<double> rdots;
-        if ((r = host_dots(c, c->gq, bs, rdots, st)) != TOPT_OK) return r;
-        const double gam = rdots[m];
+        std::vector<double> rd;
+        if ((r = host_dots(c, c->gq, bs, rd, st)) != TOPT_OK) return r;
+        const double gam = rd[m];
         std::vector<double> G(m * m), rhs(m);
         for (int i = 0; i < m; ++i) {
           const int si = win[m - 1 - i];
-          rhs[i] = gam - rdots[i];
-          for (int j = 0; j < m; ++j) {
-            const int sj = win[m - 1 - j];
-            G[i * m + j] = gam - rdots[i] - rdots[j] + H[si][sj];
-          }
+          rhs[i] = gam - rd[i];
+          for (int j = 0; j < m; ++j) G[i * m + j] = gam - rd[i] - rd[j] + H[si][win[m - 1 - j]];
         }
         std::vector<double> beta = lsq_from_gram(m, G, rhs);
         t_ls += now() - tl;
-        std::vector<const float*> vs;
-        for (int i = 0; i < m; ++i) vs.push_back(slot_a(win[m - 1 - i]));
-        launch_mix(c->q, vs.data(), beta.data(), m, V, c->vnew, st);
-        te = now();
-        if (P.model == TOPT_INCOMPRESSIBLE) {
-          PrecondArgs pa{nullptr, c->vnew, c->Z, c->vnew, nullptr, P.alpha, P.reg_order, true, c->partials,
-                         nullptr, c->cellvol};
-          launch_precond(c->g, pa, st);
+        // v^{k+1} = q + sum beta_i (q - v^{k-i})  (Alg. 3 line 9), same combination for u
+        std::vector<const float*> vs, us;
+        for (int i = 0; i < m; ++i) {
+          vs.push_back(slotA(win[m - 1 - i]));
+          us.push_back(slotU(win[m - 1 - i]));
         }
-        if ((r = eval_gradient(c, m0, m1, c->vnew, c->gnew, c->snew, c->sc + 3 * TOPT_NSCALARS, st)) != TOPT_OK)
-          return r;
-        ++grad_evals;
-        if ((r = fetch(c, 3, ns, st)) != TOPT_OK) return r;
+        launch_mix(c->q, vs.data(), beta.data(), m, V, c->vnew, st);
+        launch_mix(c->uq, us.data(), beta.data(), m, V, c->unew, st);
+        te = now();
+        if ((r = eval_new()) != TOPT_OK) return r;
         t_pde += now() - te;
-        std::swap(c->vcur, c->vnew);
-        std::swap(c->gcur, c->gnew);
-        std::swap(c->scur, c->snew);
-        cur = ns;
         ++nsteps;
       }
-      if ((r = push_ngmres(c->vcur, c->gcur)) != TOPT_OK) return r;
+      (void)wk;
+      if ((r = push(c->vcur, c->gcur, c->ucur, true)) != TOPT_OK) return r;
     } else {
-      // AA (Alg. 2): r_k = v^k - q(v^k); history of (r, q)
-      launch_sub(c->vcur, c->q, V, c->vt, st);  // r_k in vt
-      const int m = std::min((int)win.size(), wk);  // i = 1..w_k
+      // AA (Alg. 2): r_k = v^k - q(v^k); LSQ over r_k - r_{k-i}, i = 1..w_k; mix q-images
+      launch_sub(c->vcur, c->q, V, c->vt, st);  // r_k
+      const int m = std::min((int)win.size(), wk);
       if (!fp_step && m > 0) {
         const double tl = now();
         std::vector<const float*> bs;
-        for (int i = 0; i < m; ++i) bs.push_back(slot_a(win[win.size() - 1 - i]));
+        for (int i = 0; i < m; ++i) bs.push_back(slotA(win[win.size() - 1 - i]));
         bs.push_back(c->vt);
         std::vector<double> rd;
         if ((r = host_dots(c, c->vt, bs, rd, st)) != TOPT_OK) return r;
         const double gam = rd[m];
-        std::vector<double> Hm(m * m);
-        // <r_i, r_j> among history entries: recompute (m <= w small)
-        for (int i = 0; i < m; ++i) {
-          std::vector<const float*> b2;
-          for (int j = 0; j < m; ++j) b2.push_back(slot_a(win[win.size() - 1 - j]));
-          std::vector<double> row;
-          if ((r = host_dots(c, slot_a(win[win.size() - 1 - i]), b2, row, st)) != TOPT_OK) return r;
-          for (int j = 0; j < m; ++j) Hm[i * m + j] = row[j];
-        }
         std::vector<double> G(m * m), rhs(m);
         for (int i = 0; i < m; ++i) {
+          std::vector<const float*> b2;
+          for (int j = 0; j < m; ++j) b2.push_back(slotA(win[win.size() - 1 - j]));
+          std::vector<double> row;
+          if ((r = host_dots(c, slotA(win[win.size() - 1 - i]), b2, row, st)) != TOPT_OK) return r;
           rhs[i] = gam - rd[i];
-          for (int j = 0; j < m; ++j) G[i * m + j] = gam - rd[i] - rd[j] + Hm[i * m + j];
+          for (int j = 0; j < m; ++j) G[i * m + j] = gam - rd[i] - rd[j] + row[j];
         }
         std::vector<double> xi = lsq_from_gram(m, G, rhs);
         t_ls += now() - tl;
-        std::vector<const float*> qsv;
-        for (int i = 0; i < m; ++i) qsv.push_back(slot_b(win[win.size() - 1 - i]));
-        launch_mix(c->q, qsv.data(), xi.data(), m, V, c->vnew, st);
+        std::vector<const float*> qv, qu;
+        for (int i = 0; i < m; ++i) {
+          qv.push_back(slotB(win[win.size() - 1 - i]));
+          qu.push_back(slotU(win[win.size() - 1 - i]));
+        }
+        launch_mix(c->q, qv.data(), xi.data(), m, V, c->vnew, st);
+        launch_mix(c->uq, qu.data(), xi.data(), m, V, c->unew, st);
+        if ((r = push(c->vt, c->q, c->uq, false)) != TOPT_OK) return r;
+        te = now();
+        if ((r = eval_new()) != TOPT_OK) return r;
+        t_pde += now() - te;
         ++nsteps;
       } else {
-        TOPT_CUDA(cudaMemcpyAsync(c->vnew, c->q, V * 4, cudaMemcpyDeviceToDevice, st));
-      }
-      // push (r_k, q_k)
-      int slot;
-      if ((int)win.size() < W1) slot = (int)win.size();
-      else { slot = win.front(); win.pop_front(); }
-      TOPT_CUDA(cudaMemcpyAsync(slot_a(slot), c->vt, V * 4, cudaMemcpyDeviceToDevice, st));
-      TOPT_CUDA(cudaMemcpyAsync(slot_b(slot), c->q, V * 4, cudaMemcpyDeviceToDevice, st));
-      win.push_back(slot);
-      if (fp_step || m == 0) {
+        if ((r = push(c->vt, c->q, c->uq, false)) != TOPT_OK) return r;
         te = now();
         if ((r = eval_q()) != TOPT_OK) return r;
         t_pde += now() - te;
-        std::swap(c->vcur, c->q);
-        std::swap(c->gcur, c->gq);
-        std::swap(c->scur, c->sq);
-        cur = qs;
-      } else {
-        te = now();
-        if (P.model == TOPT_INCOMPRESSIBLE) {
-          PrecondArgs pa{nullptr, c->vnew, c->Z, c->vnew, nullptr, P.alpha, P.reg_order, true, c->partials,
-                         nullptr, c->cellvol};
-          launch_precond(c->g, pa, st);
-        }
-        if ((r = eval_gradient(c, m0, m1, c->vnew, c->gnew, c->snew, c->sc + 3 * TOPT_NSCALARS, st)) != TOPT_OK)
-          return r;
-        ++grad_evals;
-        if ((r = fetch(c, 3, ns, st)) != TOPT_OK) return r;
-        t_pde += now() - te;
-        std::swap(c->vcur, c->vnew);
-        std::swap(c->gcur, c->gnew);
-        std::swap(c->scur, c->snew);
-        cur = ns;
+        accept_q();
       }
     }
     ++k;
-    const double gi = cur.v[TOPT_S_GRAD_INF];
-    if (!std::isfinite(gi) || !std::isfinite(cur.v[TOPT_S_OBJ]))
+    const double gi = cur.pub(TOPT_S_GRAD_INF);
+    if (!std::isfinite(gi) || !std::isfinite(cur.pub(TOPT_S_OBJ)))
       return fail(TOPT_ERR_CUDA, "non-finite objective or gradient");
     if (gi <= P.eps_rel * g0) {
       exit_code = TOPT_CONVERGED;
@@ -825,10 +854,10 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
   }
   TOPT_CUDA(cudaMemcpyAsync(v_inout, c->vcur, V * 4, cudaMemcpyDeviceToDevice, st));
   TOPT_CUDA(cudaStreamSynchronize(st));
-  rep->obj = cur.v[TOPT_S_OBJ];
-  rep->dist = cur.v[TOPT_S_DIST];
-  rep->reg = cur.v[TOPT_S_REG];
-  rep->grad_inf = cur.v[TOPT_S_GRAD_INF];
+  rep->obj = cur.pub(TOPT_S_OBJ);
+  rep->dist = cur.pub(TOPT_S_DIST);
+  rep->reg = cur.pub(TOPT_S_REG);
+  rep->grad_inf = cur.pub(TOPT_S_GRAD_INF);
   rep->rho = rho;
   rep->iters = k;
   rep->grad_evals = grad_evals;

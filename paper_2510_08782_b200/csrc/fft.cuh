@@ -1,8 +1,9 @@
-// fft.cuh — block-cooperative radix-16/8/4/2 Stockham FFT of lines held in shared memory.
+// fft.cuh — block-cooperative radix-16/8/4/2 Stockham FFT of lines held in shared memory,
+// in fp32 (float2) or fp64 (double2) arithmetic.
 //
 // Used by every spectral kernel of the hot path: the pseudo-spectral derivatives
-// (reading R3) and the 3D FFT of the preconditioner
-// (alpha L)^{-1}.  N = 2^p, 4 <= N <= 1024.
+// (reading R3) and the 3D FFTs of the preconditioner
+// (alpha L)^{-1} and of alpha L v.  N = 2^p, 8 <= N <= 1024.
 //
 // A line of N complex values is transformed in place in shared memory by
 // T = max(1, N/16) threads; every stage loads 16 values per thread, applies the
@@ -10,147 +11,138 @@
 // radix R = min(16, N/Ns), and writes back in Stockham (auto-sort) order:
 //   j in [0, N/R), k = j mod Ns:  a_r = x[j + r N/R] * W^{r k N/(Ns R)},
 //   a = DFT_R(a),  x'[(j/Ns) Ns R + k + q Ns] = a_q .
-// Shared memory lines are padded by one float2 every 16 entries (bank conflicts).
+// Shared-memory lines are padded by one element every 16 entries (bank conflicts).
+//
+// This header DEFINES the device twiddle tables: include it from ONE translation unit.
 #pragma once
 #include <cuda_runtime.h>
 
 namespace topt {
 
-__host__ __device__ constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n / 2); }
 __host__ __device__ constexpr int fft_threads(int n) { return n >= 16 ? n / 16 : 1; }
 __host__ __device__ constexpr int fft_pad(int i) { return i + (i >> 4); }
 __host__ __device__ constexpr int fft_line_stride(int n) { return n + n / 16 + 1; }
 
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
-}
-__device__ __forceinline__ float2 cmulconj(float2 a, float2 b) {  // a * conj(b)
-  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
-}
+template <typename C> struct Real;
+template <> struct Real<float2> { using T = float; };
+template <> struct Real<double2> { using T = double; };
+
+__device__ __forceinline__ float2 mk(float x, float y) { return make_float2(x, y); }
+__device__ __forceinline__ double2 mk(double x, double y) { return make_double2(x, y); }
+
+template <typename C>
+__device__ __forceinline__ C cadd(C a, C b) { return mk(a.x + b.x, a.y + b.y); }
+template <typename C>
+__device__ __forceinline__ C csub(C a, C b) { return mk(a.x - b.x, a.y - b.y); }
+template <typename C>
+__device__ __forceinline__ C cmul(C a, C b) { return mk(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x)); }
+template <typename C>
+__device__ __forceinline__ C cmulconj(C a, C b) { return mk(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y)); }
 // multiply by -i (forward) or +i (inverse)
-template <bool INV>
-__device__ __forceinline__ float2 mul_mi(float2 a) {
-  return INV ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
-}
-// multiply by W_R^m = exp(-+ 2 pi i m / R) given cos/sin of 2 pi m / R
-template <bool INV>
-__device__ __forceinline__ float2 mul_w(float2 a, float c, float s) {
-  return INV ? make_float2(a.x * c - a.y * s, a.x * s + a.y * c)
-             : make_float2(a.x * c + a.y * s, a.y * c - a.x * s);
+template <bool INV, typename C>
+__device__ __forceinline__ C mul_mi(C a) { return INV ? mk(-a.y, a.x) : mk(a.y, -a.x); }
+// multiply by W = exp(-+ 2 pi i m / R) given cos, sin of 2 pi m / R
+template <bool INV, typename C>
+__device__ __forceinline__ C mul_w(C a, typename Real<C>::T c, typename Real<C>::T s) {
+  return INV ? mk(a.x * c - a.y * s, a.x * s + a.y * c) : mk(a.x * c + a.y * s, a.y * c - a.x * s);
 }
 
-template <bool INV>
-__device__ __forceinline__ void dft2(float2& a0, float2& a1) {
-  float2 t = csub(a0, a1);
+template <bool INV, typename C>
+__device__ __forceinline__ void dft2(C& a0, C& a1) {
+  C t = csub(a0, a1);
   a0 = cadd(a0, a1);
   a1 = t;
 }
 
-template <bool INV>
-__device__ __forceinline__ void dft4(float2& a0, float2& a1, float2& a2, float2& a3) {
-  float2 t0 = cadd(a0, a2), t1 = csub(a0, a2), t2 = cadd(a1, a3), t3 = mul_mi<INV>(csub(a1, a3));
+template <bool INV, typename C>
+__device__ __forceinline__ void dft4(C& a0, C& a1, C& a2, C& a3) {
+  C t0 = cadd(a0, a2), t1 = csub(a0, a2), t2 = cadd(a1, a3), t3 = mul_mi<INV>(csub(a1, a3));
   a0 = cadd(t0, t2);
   a2 = csub(t0, t2);
   a1 = cadd(t1, t3);
   a3 = csub(t1, t3);
 }
 
-// cos / sin (2 pi m / 16), m = 0..15
-#define TOPT_C16_1 0.92387953251128674f
-#define TOPT_S16_1 0.38268343236508978f
-#define TOPT_R2 0.70710678118654752f
-
-template <bool INV>
-__device__ __forceinline__ float2 w16(float2 a, int m) {  // m compile-time after unrolling
+// W_16^m, m = n2*k1 in 0..9 (compile-time after unrolling)
+template <bool INV, typename C>
+__device__ __forceinline__ C w16(C a, int m) {
+  using T = typename Real<C>::T;
+  const T c1 = (T)0.92387953251128675613, s1 = (T)0.38268343236508977173, r2 = (T)0.70710678118654752440;
   switch (m & 15) {
     case 0: return a;
-    case 1: return mul_w<INV>(a, TOPT_C16_1, TOPT_S16_1);
-    case 2: return mul_w<INV>(a, TOPT_R2, TOPT_R2);
-    case 3: return mul_w<INV>(a, TOPT_S16_1, TOPT_C16_1);
+    case 1: return mul_w<INV>(a, c1, s1);
+    case 2: return mul_w<INV>(a, r2, r2);
+    case 3: return mul_w<INV>(a, s1, c1);
     case 4: return mul_mi<INV>(a);
-    case 5: return mul_w<INV>(a, -TOPT_S16_1, TOPT_C16_1);
-    case 6: return mul_w<INV>(a, -TOPT_R2, TOPT_R2);
-    case 7: return mul_w<INV>(a, -TOPT_C16_1, TOPT_S16_1);
-    case 8: return make_float2(-a.x, -a.y);
-    case 9: return mul_w<INV>(a, -TOPT_C16_1, -TOPT_S16_1);
-    default: return a;  // not reached for radix 16 (n2*k1 <= 9)
+    case 5: return mul_w<INV>(a, -s1, c1);
+    case 6: return mul_w<INV>(a, -r2, r2);
+    case 7: return mul_w<INV>(a, -c1, s1);
+    case 8: return mk(-a.x, -a.y);
+    case 9: return mul_w<INV>(a, -c1, -s1);
+    default: return a;
   }
 }
 
-// In-register DFT of size R on a[0..R-1], natural order in and out.
-template <int R, bool INV>
-__device__ __forceinline__ void dft(float2* a);
-
-template <>
-__device__ __forceinline__ void dft<1, false>(float2*) {}
-template <>
-__device__ __forceinline__ void dft<1, true>(float2*) {}
-template <>
-__device__ __forceinline__ void dft<2, false>(float2* a) { dft2<false>(a[0], a[1]); }
-template <>
-__device__ __forceinline__ void dft<2, true>(float2* a) { dft2<true>(a[0], a[1]); }
-template <>
-__device__ __forceinline__ void dft<4, false>(float2* a) { dft4<false>(a[0], a[1], a[2], a[3]); }
-template <>
-__device__ __forceinline__ void dft<4, true>(float2* a) { dft4<true>(a[0], a[1], a[2], a[3]); }
-
+template <int R, bool INV, typename C>
+struct Dft;
+template <bool INV, typename C>
+struct Dft<1, INV, C> { static __device__ __forceinline__ void run(C*) {} };
+template <bool INV, typename C>
+struct Dft<2, INV, C> { static __device__ __forceinline__ void run(C* a) { dft2<INV>(a[0], a[1]); } };
+template <bool INV, typename C>
+struct Dft<4, INV, C> {
+  static __device__ __forceinline__ void run(C* a) { dft4<INV>(a[0], a[1], a[2], a[3]); }
+};
 // 8 = 4 x 2: n = 2 n1 + n2, k = k1 + 4 k2
-template <bool INV>
-__device__ __forceinline__ void dft8_impl(float2* a) {
-  float2 y0[4] = {a[0], a[2], a[4], a[6]};
-  float2 y1[4] = {a[1], a[3], a[5], a[7]};
-  dft4<INV>(y0[0], y0[1], y0[2], y0[3]);
-  dft4<INV>(y1[0], y1[1], y1[2], y1[3]);
-  y1[1] = w16<INV>(y1[1], 2);
-  y1[2] = w16<INV>(y1[2], 4);
-  y1[3] = w16<INV>(y1[3], 6);
+template <bool INV, typename C>
+struct Dft<8, INV, C> {
+  static __device__ __forceinline__ void run(C* a) {
+    C y0[4] = {a[0], a[2], a[4], a[6]};
+    C y1[4] = {a[1], a[3], a[5], a[7]};
+    dft4<INV>(y0[0], y0[1], y0[2], y0[3]);
+    dft4<INV>(y1[0], y1[1], y1[2], y1[3]);
+    y1[1] = w16<INV>(y1[1], 2);
+    y1[2] = w16<INV>(y1[2], 4);
+    y1[3] = w16<INV>(y1[3], 6);
 #pragma unroll
-  for (int k1 = 0; k1 < 4; ++k1) {
-    a[k1] = cadd(y0[k1], y1[k1]);
-    a[k1 + 4] = csub(y0[k1], y1[k1]);
+    for (int k1 = 0; k1 < 4; ++k1) {
+      a[k1] = cadd(y0[k1], y1[k1]);
+      a[k1 + 4] = csub(y0[k1], y1[k1]);
+    }
   }
-}
-template <>
-__device__ __forceinline__ void dft<8, false>(float2* a) { dft8_impl<false>(a); }
-template <>
-__device__ __forceinline__ void dft<8, true>(float2* a) { dft8_impl<true>(a); }
-
+};
 // 16 = 4 x 4: n = 4 n1 + n2, k = k1 + 4 k2
-template <bool INV>
-__device__ __forceinline__ void dft16_impl(float2* a) {
-  float2 y[4][4];
+template <bool INV, typename C>
+struct Dft<16, INV, C> {
+  static __device__ __forceinline__ void run(C* a) {
+    C y[4][4];
 #pragma unroll
-  for (int n2 = 0; n2 < 4; ++n2) {
-    y[n2][0] = a[n2]; y[n2][1] = a[4 + n2]; y[n2][2] = a[8 + n2]; y[n2][3] = a[12 + n2];
-    dft4<INV>(y[n2][0], y[n2][1], y[n2][2], y[n2][3]);
+    for (int n2 = 0; n2 < 4; ++n2) {
+      y[n2][0] = a[n2]; y[n2][1] = a[4 + n2]; y[n2][2] = a[8 + n2]; y[n2][3] = a[12 + n2];
+      dft4<INV>(y[n2][0], y[n2][1], y[n2][2], y[n2][3]);
+    }
+#pragma unroll
+    for (int n2 = 1; n2 < 4; ++n2)
+#pragma unroll
+      for (int k1 = 1; k1 < 4; ++k1) y[n2][k1] = w16<INV>(y[n2][k1], n2 * k1);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      C b0 = y[0][k1], b1 = y[1][k1], b2 = y[2][k1], b3 = y[3][k1];
+      dft4<INV>(b0, b1, b2, b3);
+      a[k1] = b0; a[k1 + 4] = b1; a[k1 + 8] = b2; a[k1 + 12] = b3;
+    }
   }
-#pragma unroll
-  for (int n2 = 1; n2 < 4; ++n2)
-#pragma unroll
-    for (int k1 = 1; k1 < 4; ++k1) y[n2][k1] = w16<INV>(y[n2][k1], n2 * k1);
-#pragma unroll
-  for (int k1 = 0; k1 < 4; ++k1) {
-    float2 b0 = y[0][k1], b1 = y[1][k1], b2 = y[2][k1], b3 = y[3][k1];
-    dft4<INV>(b0, b1, b2, b3);
-    a[k1] = b0; a[k1 + 4] = b1; a[k1 + 8] = b2; a[k1 + 12] = b3;
-  }
-}
-template <>
-__device__ __forceinline__ void dft<16, false>(float2* a) { dft16_impl<false>(a); }
-template <>
-__device__ __forceinline__ void dft<16, true>(float2* a) { dft16_impl<true>(a); }
+};
 
-// One Stockham stage on a padded line `buf` (stride fft_pad), done by T threads (tid < T).
-// tw: table of exp(-2 pi i m / N), m = 0..N-1 (padded indexing not used for the table).
-// All threads of the block must call it (it contains __syncthreads) — `active` masks work.
-template <int N, int R, int NS, bool INV>
-__device__ __forceinline__ void fft_stage(float2* buf, const float2* tw, int tid, bool active) {
+// One Stockham stage on a padded line `buf`, done by T threads (tid < T).
+// tw: table of exp(-2 pi i m / N), m = 0..N-1.
+// All threads of the block must call it (it contains __syncthreads); `active` masks work.
+template <int N, int R, int NS, bool INV, typename C>
+__device__ __forceinline__ void fft_stage(C* buf, const C* tw, int tid, bool active) {
   constexpr int M = N / R;
   constexpr int T = fft_threads(N);
   constexpr int NB = M / T;  // butterflies per thread
-  float2 a[NB][R];
+  C a[NB][R];
   if (active) {
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
@@ -161,11 +153,11 @@ __device__ __forceinline__ void fft_stage(float2* buf, const float2* tw, int tid
       if (NS > 1) {
 #pragma unroll
         for (int r = 1; r < R; ++r) {
-          const float2 w = tw[(r * k * (N / (NS * R))) & (N - 1)];
+          const C w = tw[(r * k * (N / (NS * R))) & (N - 1)];
           a[b][r] = INV ? cmulconj(a[b][r], w) : cmul(a[b][r], w);
         }
       }
-      dft<R, INV>(a[b]);
+      Dft<R, INV, C>::run(a[b]);
     }
   }
   __syncthreads();
@@ -182,34 +174,38 @@ __device__ __forceinline__ void fft_stage(float2* buf, const float2* tw, int tid
   __syncthreads();
 }
 
-template <int N, int NS, bool INV>
+template <int N, int NS, bool INV, typename C>
 struct FftStages {
-  static __device__ __forceinline__ void run(float2* buf, const float2* tw, int tid, bool active) {
+  static __device__ __forceinline__ void run(C* buf, const C* tw, int tid, bool active) {
     constexpr int REM = N / NS;
     constexpr int R = REM >= 16 ? 16 : REM;
-    fft_stage<N, R, NS, INV>(buf, tw, tid, active);
-    FftStages<N, NS * R, INV>::run(buf, tw, tid, active);
+    fft_stage<N, R, NS, INV, C>(buf, tw, tid, active);
+    FftStages<N, NS * R, INV, C>::run(buf, tw, tid, active);
   }
 };
-template <int N, bool INV>
-struct FftStages<N, N, INV> {
-  static __device__ __forceinline__ void run(float2*, const float2*, int, bool) {}
+template <int N, bool INV, typename C>
+struct FftStages<N, N, INV, C> {
+  static __device__ __forceinline__ void run(C*, const C*, int, bool) {}
 };
 
 // Unnormalised DFT (forward: exp(-i k x), inverse: exp(+i k x)) of a padded smem line.
-template <int N, bool INV>
-__device__ __forceinline__ void fft_line(float2* buf, const float2* tw, int tid, bool active) {
-  FftStages<N, 1, INV>::run(buf, tw, tid, active);
+template <int N, bool INV, typename C>
+__device__ __forceinline__ void fft_line(C* buf, const C* tw, int tid, bool active) {
+  FftStages<N, 1, INV, C>::run(buf, tw, tid, active);
 }
 
-// Device twiddle tables: g_twiddle[N + m] = exp(-2 pi i m / N) for N = 4..1024 (fp64-rounded),
-// filled by upload_twiddles(). Defined here: include this header from ONE translation unit.
+// Device twiddle tables: tw[N + m] = exp(-2 pi i m / N), N = 4..1024, computed in fp64
+// on the host (upload_twiddles) and rounded once to the table's precision.
 __device__ float2 g_twiddle[2048];
+__device__ double2 g_twiddle_d[2048];
 
-// Copy the twiddle table of size N into shared memory (all threads).
 template <int N>
 __device__ __forceinline__ void load_twiddles(float2* s_tw) {
   for (int i = threadIdx.x; i < N; i += blockDim.x) s_tw[i] = g_twiddle[N + i];
+}
+template <int N>
+__device__ __forceinline__ void load_twiddles(double2* s_tw) {
+  for (int i = threadIdx.x; i < N; i += blockDim.x) s_tw[i] = g_twiddle_d[N + i];
 }
 
 }  // namespace topt

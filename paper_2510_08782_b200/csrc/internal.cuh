@@ -39,7 +39,9 @@ struct VecList { const float* p[kMaxVecs]; float c[kMaxVecs]; };
 void upload_twiddles();
 
 // ---- semi-Lagrangian kernels (kernels_sl.cu) --------------------------------------
-void launch_trace(const Geom& g, const float* v, float* df, float* da, cudaStream_t st);
+// Feet; when vsum_partials != null also per-block sums of v_c into slots 0..d-1 (*nparts blocks)
+void launch_trace(const Geom& g, const float* v, float* df, float* da, double* vsum_partials, int* nparts,
+                  cudaStream_t st);
 // out = I[in](l + delta) (* E if E != nullptr)
 void launch_sl_step(const Geom& g, const float* in, const float* delta, const float* E, float* out,
                     cudaStream_t st);
@@ -64,24 +66,17 @@ struct DerivArgs {
 };
 void launch_deriv_accum(const Geom& g, int axis, const DerivArgs& a, cudaStream_t st);
 
-// Preconditioner / projection passes on Z_c = v_c + i b_c (c < d):
-//   g = alpha L v + b   (Leray if leray), s = -(alpha L~)^{-1} g
-// Outputs g, s (either may be null), fp64 partials for ||g||_inf, <g,s>, and the
-// spectral sums reg, <s,Lv>, <s,Ls>.
-struct PrecondArgs {
-  const float* v;     // d*F or null (treated as 0)
-  const float* b;     // d*F or null (treated as 0)
-  float2* Z;          // d*F complex workspace
-  float* g;           // d*F or null
-  float* s;           // d*F or null
-  double alpha;
-  int p;              // reg order
-  bool leray;
-  double* partials;   // reduction buffer
-  double* scalars;    // device scalars
-  double cellvol;     // h^d
-};
-void launch_precond(const Geom& g, const PrecondArgs& a, cudaStream_t st);
+// u = alpha L v (fp64 chain; Zv = 2 double2 fields of F)
+void launch_vchain(const Geom& g, const float* v, double2* Zv, float* u, double alpha, int p, cudaStream_t st);
+// b-chain up to the x^-1 pass (Zb = 3 float2 fields of F); see kernels_spectral.cu
+void launch_bchain(const Geom& g, const float* b, float2* Zb, double alpha, int p, bool leray, cudaStream_t st);
+// x^-1 of the b-chain and pointwise assembly g = u + b_L, s = -(v - vbar) + p, with
+// partial sums in slots 0..9 (max|g|, sum gs, sum vu, sum su, sum g_c (3), sum s_c (3)).
+void launch_assemble(const Geom& g, const float2* Zb, bool leray, const float* b, const float* u, const float* v,
+                     const double* vsum, float* gout, float* sout, double* partials, int* nparts, cudaStream_t st);
+
+// Internal scalars (per evaluation, device): sums used to finish the public scalars.
+enum { I_SUMV = 0, I_GMAX = 3, I_GS = 4, I_VU = 5, I_SU = 6, I_SUMG = 7, I_SUMS = 10, I_COUNT = 16 };
 
 // ---- vector kernels (kernels_vec.cu) ------------------------------------------------
 void launch_finalize(const double* partials, int slot, int nparts, double scale, bool is_max,
@@ -90,11 +85,18 @@ void launch_finalize(const double* partials, int slot, int nparts, double scale,
 void launch_finalize_multi(const double* partials, int slot0, int nslots, int nparts, double scale,
                            double* dst, cudaStream_t st);
 void launch_combine_obj(double* scalars, cudaStream_t st);  // OBJ = DIST + REG
+// finalize slots [first, first+count) (slot 0 of the assembly = max) into dst
+void launch_finalize_slots(const double* partials, int first, int count, int nparts, bool first_is_max,
+                           double* dst, cudaStream_t st);
+// public scalars from the internal sums (see kernels_vec.cu)
+void launch_finish(const double* isc, double* sc, int d, double n, double cellvol, cudaStream_t st);
 void launch_multidot(const float* a, const float* const* bs, int count, size_t n, double* partials,
                      int* nparts, cudaStream_t st);
 void launch_mix(const float* q, const float* const* vs, const double* beta, int count, size_t n,
                 float* out, cudaStream_t st);
 void launch_axpy(const float* x, float a, const float* y, size_t n, float* out, cudaStream_t st);  // out = x + a*y
 void launch_sub(const float* a, const float* b, size_t n, float* out, cudaStream_t st);           // out = a - b
+void launch_axpy_c(const float* x, float a, const float* y, size_t n, int ncomp, const float* cst, float* out,
+                   cudaStream_t st);  // out = x + a*y + cst[component]
 
 }  // namespace topt

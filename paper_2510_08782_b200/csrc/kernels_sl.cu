@@ -82,15 +82,34 @@ __device__ __forceinline__ void coords(const Geom& g, size_t i, int& x, int& y, 
   z = (int)(i >> (g.lx + g.ly));
 }
 
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double sh[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r += sh[w];
+  return r;  // valid on thread 0
+}
+
 // K1: midpoint-RK2 feet (R6), in cells.  delta_f = -c I[v](l - c v/2), delta_a = +c I[v](l + c v/2)
+// Optionally per-block sums of v_c (fp64) into partials[c * kMaxPartials + block].
 template <int D>
 __global__ void __launch_bounds__(kThreads) k_trace(Geom g, const float* __restrict__ v,
-                                                    float* __restrict__ df, float* __restrict__ da) {
+                                                    float* __restrict__ df, float* __restrict__ da,
+                                                    double* __restrict__ vsum) {
   const size_t F = g.F;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < F; i += (size_t)gridDim.x * blockDim.x) {
     int x, y, z;
     coords(g, i, x, y, z);
-    const float u0 = v[i] * g.cx, u1 = v[F + i] * g.cy, u2 = D == 3 ? v[2 * F + i] * g.cz : 0.0f;
+    const float w0 = v[i], w1 = v[F + i], w2 = D == 3 ? v[2 * F + i] : 0.0f;
+    s0 += w0; s1 += w1; s2 += w2;
+    const float u0 = w0 * g.cx, u1 = w1 * g.cy, u2 = w2 * g.cz;
 #pragma unroll
     for (int side = 0; side < 2; ++side) {
       float* out = side == 0 ? df : da;
@@ -101,6 +120,16 @@ __global__ void __launch_bounds__(kThreads) k_trace(Geom g, const float* __restr
       out[i] = sg * g.cx * st.apply(v);
       out[F + i] = sg * g.cy * st.apply(v + F);
       if (D == 3) out[2 * F + i] = sg * g.cz * st.apply(v + 2 * F);
+    }
+  }
+  if (vsum) {
+    const double a = block_sum(s0);
+    const double b = block_sum(s1);
+    const double c = block_sum(s2);
+    if (threadIdx.x == 0) {
+      vsum[blockIdx.x] = a;
+      vsum[kMaxPartials + blockIdx.x] = b;
+      vsum[2 * kMaxPartials + blockIdx.x] = c;
     }
   }
 }
@@ -121,20 +150,6 @@ __global__ void __launch_bounds__(kThreads) k_sl_step(Geom g, const float* __res
     if (HAS_E) r *= E[i];
     out[i] = r;
   }
-}
-
-__device__ __forceinline__ double block_sum(double v) {
-  __shared__ double sh[32];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) sh[wid] = v;
-  __syncthreads();
-  double r = 0.0;
-  if (threadIdx.x == 0)
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r += sh[w];
-  return r;  // valid on thread 0
 }
 
 // K3: last forward step + mismatch: mS, lamS = m1 - mS (R1), partial sum (mS - m1)^2
@@ -188,9 +203,12 @@ int grid_for(size_t n, int threads, int max_blocks) {
 
 static int sl_grid(const Geom& g) { return grid_for(g.F, kThreads, 148 * 16); }
 
-void launch_trace(const Geom& g, const float* v, float* df, float* da, cudaStream_t st) {
-  if (g.d == 3) k_trace<3><<<sl_grid(g), kThreads, 0, st>>>(g, v, df, da);
-  else k_trace<2><<<sl_grid(g), kThreads, 0, st>>>(g, v, df, da);
+void launch_trace(const Geom& g, const float* v, float* df, float* da, double* vsum_partials, int* nparts,
+                  cudaStream_t st) {
+  const int gr = sl_grid(g);
+  if (nparts) *nparts = gr;
+  if (g.d == 3) k_trace<3><<<gr, kThreads, 0, st>>>(g, v, df, da, vsum_partials);
+  else k_trace<2><<<gr, kThreads, 0, st>>>(g, v, df, da, vsum_partials);
 }
 
 void launch_sl_step(const Geom& g, const float* in, const float* delta, const float* E, float* out,

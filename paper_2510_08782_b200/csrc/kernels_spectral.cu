@@ -27,20 +27,23 @@ namespace topt {
 
 
 void upload_twiddles() {
-  static float2 host[2048];
+  static float2 hf[2048];
+  static double2 hd[2048];
   for (int N = 4; N <= 1024; N *= 2)
     for (int m = 0; m < N; ++m) {
       const double a = -2.0 * M_PI * (double)m / (double)N;
-      host[N + m] = make_float2((float)cos(a), (float)sin(a));
+      hd[N + m] = make_double2(cos(a), sin(a));
+      hf[N + m] = make_float2((float)cos(a), (float)sin(a));
     }
-  cudaMemcpyToSymbol(g_twiddle, host, sizeof(host));
+  cudaMemcpyToSymbol(g_twiddle, hf, sizeof(hf));
+  cudaMemcpyToSymbol(g_twiddle_d, hd, sizeof(hd));
 }
 
 template <int N>
 struct LineCfg {
   static constexpr int T = fft_threads(N);
   static constexpr int LPB = kThreads / T;           // complex lines per 256-thread block
-  static constexpr int STRIDE = fft_line_stride(N);  // float2 per smem line
+  static constexpr int STRIDE = fft_line_stride(N);  // complex elements per smem line
 };
 
 __device__ __forceinline__ int paired_pos(int q, int N) {  // natural index -> paired position
@@ -279,373 +282,404 @@ void launch_deriv_accum(const Geom& g, int axis, const DerivArgs& a, cudaStream_
 }
 
 // =====================================================================================
-// Preconditioner passes.
+// Preconditioner / regulariser chains (3D FFT = x pass, [y pass], last-axis pass with a
+// fused spectral operator, [y^-1], x^-1).  Spectra stay in natural order.
+//
+//  v-chain (fp64 arithmetic AND fp64 intermediates): u = alpha L v.  L = |k|^{2p}
+//    amplifies any rounding at high |k| by up to (k_max/k)^{2p}, so the chain that
+//    applies it runs in double; packing v_x + i v_y is exact because
+//    alpha L(k) is real and even.
+//  b-chain (fp32): the smoothing inverse -(alpha L~)^{-1} and the Leray projector are
+//    well conditioned.  Non-Leray: Z0 = b_x + i b_y, Z1 = b_z -> W = -Z/(alpha L~ n) gives
+//    p = -(alpha L~)^{-1} b.  Leray: Z_c = b_c (real) -> W_c = (P_L b^ + i p^)/n with
+//    p^ = -P_L b^ / (alpha L~) (pointwise in k across components, R3/R9).
 // =====================================================================================
+template <typename C>
+struct ZList { C* z[3]; };
+struct RealIn { const float* re[3]; const float* im[3]; };
 
-// Forward x pass: Z[row][pos(q)] = FFT_x(v + i b)[q]   (rows = ny*nz, one complex line per row)
-template <int N>
-__global__ void __launch_bounds__(kThreads) k_px_fwd(Geom g, const float* __restrict__ v,
-                                                     const float* __restrict__ b,
-                                                     float2* __restrict__ Z) {
-  using C = LineCfg<N>;
-  extern __shared__ float2 smem[];
-  float2* buf = smem;
-  float2* tw = smem + C::LPB * C::STRIDE;
+// x pass forward: Z_f[row][q] = FFT_x(re_f + i im_f)[q]
+template <int N, typename C>
+__global__ void __launch_bounds__(kThreads) k_px_fwd(Geom g, RealIn in, ZList<C> Z) {
+  using L = LineCfg<N>;
+  using T = typename Real<C>::T;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C* buf = reinterpret_cast<C*>(smraw);
+  C* tw = buf + L::LPB * L::STRIDE;
   load_twiddles<N>(tw);
   const size_t nrows = (size_t)g.ny * g.nz;
-  const size_t row0 = (size_t)blockIdx.x * C::LPB;
-  const int comp = blockIdx.y;
-  const float* vc = v ? v + comp * g.F : nullptr;
-  const float* bc = b ? b + comp * g.F : nullptr;
-  float2* Zc = Z + comp * g.F;
-  const int n4 = C::LPB * N / 4;
+  const size_t row0 = (size_t)blockIdx.x * L::LPB;
+  const int f = blockIdx.y;
+  const float* re = in.re[f];
+  const float* im = in.im[f];
+  C* Zf = Z.z[f];
+  const int n4 = L::LPB * N / 4;
   for (int f4 = threadIdx.x; f4 < n4; f4 += kThreads) {
     const int rl = (f4 * 4) / N, pos = (f4 * 4) % N;
     const size_t gi = (row0 + rl) * N + pos;
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), c = a;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
     if (row0 + rl < nrows) {
-      if (vc) a = *reinterpret_cast<const float4*>(vc + gi);
-      if (bc) c = *reinterpret_cast<const float4*>(bc + gi);
+      if (re) a = *reinterpret_cast<const float4*>(re + gi);
+      if (im) b = *reinterpret_cast<const float4*>(im + gi);
     }
-    float2* L = buf + rl * C::STRIDE;
-    L[fft_pad(pos + 0)] = make_float2(a.x, c.x);
-    L[fft_pad(pos + 1)] = make_float2(a.y, c.y);
-    L[fft_pad(pos + 2)] = make_float2(a.z, c.z);
-    L[fft_pad(pos + 3)] = make_float2(a.w, c.w);
+    C* Ln = buf + rl * L::STRIDE;
+    Ln[fft_pad(pos + 0)] = mk((T)a.x, (T)b.x);
+    Ln[fft_pad(pos + 1)] = mk((T)a.y, (T)b.y);
+    Ln[fft_pad(pos + 2)] = mk((T)a.z, (T)b.z);
+    Ln[fft_pad(pos + 3)] = mk((T)a.w, (T)b.w);
   }
   __syncthreads();
-  const int myline = threadIdx.x / C::T, tid = threadIdx.x % C::T;
-  fft_line<N, false>(buf + myline * C::STRIDE, tw, tid, myline < C::LPB);
-  for (int i = threadIdx.x; i < C::LPB * N; i += kThreads) {
-    const int rl = i / N, p = i % N;
-    if (row0 + rl < nrows) Zc[(row0 + rl) * N + p] = buf[rl * C::STRIDE + fft_pad(paired_q(p, N))];
+  const int myline = threadIdx.x / L::T, tid = threadIdx.x % L::T;
+  fft_line<N, false>(buf + myline * L::STRIDE, tw, tid, myline < L::LPB);
+  for (int i = threadIdx.x; i < L::LPB * N; i += kThreads) {
+    const int rl = i / N, q = i % N;
+    if (row0 + rl < nrows) Zf[(row0 + rl) * N + q] = buf[rl * L::STRIDE + fft_pad(q)];
   }
 }
 
-// Inverse x pass: g + i s = IFFT_x(Z) (paired order in), reductions max|g|, sum g*s.
-template <int N>
-__global__ void __launch_bounds__(kThreads) k_px_inv(Geom g, const float2* __restrict__ Z,
-                                                     float* __restrict__ gout, float* __restrict__ sout,
-                                                     double* __restrict__ partials, int pstride) {
-  using C = LineCfg<N>;
-  extern __shared__ float2 smem[];
-  float2* buf = smem;
-  float2* tw = smem + C::LPB * C::STRIDE;
+// x pass inverse to real outputs: re_f + i im_f = IFFT_x(Z_f)  (either output may be null)
+struct RealOut { float* re[3]; float* im[3]; };
+template <int N, typename C>
+__global__ void __launch_bounds__(kThreads) k_px_inv(Geom g, ZList<C> Z, RealOut out) {
+  using L = LineCfg<N>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C* buf = reinterpret_cast<C*>(smraw);
+  C* tw = buf + L::LPB * L::STRIDE;
   load_twiddles<N>(tw);
   const size_t nrows = (size_t)g.ny * g.nz;
-  const size_t row0 = (size_t)blockIdx.x * C::LPB;
-  const int comp = blockIdx.y;
-  const float2* Zc = Z + comp * g.F;
-  for (int i = threadIdx.x; i < C::LPB * N; i += kThreads) {
-    const int rl = i / N, p = i % N;
-    float2 z = make_float2(0.f, 0.f);
-    if (row0 + rl < nrows) z = Zc[(row0 + rl) * N + p];
-    buf[rl * C::STRIDE + fft_pad(paired_q(p, N))] = z;
+  const size_t row0 = (size_t)blockIdx.x * L::LPB;
+  const int f = blockIdx.y;
+  const C* Zf = Z.z[f];
+  for (int i = threadIdx.x; i < L::LPB * N; i += kThreads) {
+    const int rl = i / N, q = i % N;
+    C z = mk((typename Real<C>::T)0, (typename Real<C>::T)0);
+    if (row0 + rl < nrows) z = Zf[(row0 + rl) * N + q];
+    buf[rl * L::STRIDE + fft_pad(q)] = z;
   }
   __syncthreads();
-  const int myline = threadIdx.x / C::T, tid = threadIdx.x % C::T;
-  fft_line<N, true>(buf + myline * C::STRIDE, tw, tid, myline < C::LPB);
-  double gmax = 0.0, gs = 0.0;
-  const int n4 = C::LPB * N / 4;
+  const int myline = threadIdx.x / L::T, tid = threadIdx.x % L::T;
+  fft_line<N, true>(buf + myline * L::STRIDE, tw, tid, myline < L::LPB);
+  float* re = out.re[f];
+  float* im = out.im[f];
+  const int n4 = L::LPB * N / 4;
   for (int f4 = threadIdx.x; f4 < n4; f4 += kThreads) {
     const int rl = (f4 * 4) / N, pos = (f4 * 4) % N;
     if (row0 + rl >= nrows) continue;
-    const size_t gi = comp * g.F + (row0 + rl) * N + pos;
-    const float2* L = buf + rl * C::STRIDE;
-    const float2 a0 = L[fft_pad(pos)], a1 = L[fft_pad(pos + 1)], a2 = L[fft_pad(pos + 2)],
-                 a3 = L[fft_pad(pos + 3)];
-    if (gout) *reinterpret_cast<float4*>(gout + gi) = make_float4(a0.x, a1.x, a2.x, a3.x);
-    if (sout) *reinterpret_cast<float4*>(sout + gi) = make_float4(a0.y, a1.y, a2.y, a3.y);
-    gmax = fmax(gmax, (double)fmaxf(fmaxf(fabsf(a0.x), fabsf(a1.x)), fmaxf(fabsf(a2.x), fabsf(a3.x))));
-    gs += (double)(a0.x * a0.y) + (double)(a1.x * a1.y) + (double)(a2.x * a2.y) + (double)(a3.x * a3.y);
-  }
-  // block reductions (max, sum) in fixed order
-  __shared__ double shm[32], shs[32];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    gmax = fmax(gmax, __shfl_down_sync(0xffffffffu, gmax, o));
-    gs += __shfl_down_sync(0xffffffffu, gs, o);
-  }
-  if ((threadIdx.x & 31) == 0) { shm[threadIdx.x >> 5] = gmax; shs[threadIdx.x >> 5] = gs; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double m = 0.0, s = 0.0;
-    for (int w = 0; w < kThreads / 32; ++w) { m = fmax(m, shm[w]); s += shs[w]; }
-    const int bid = blockIdx.y * gridDim.x + blockIdx.x;
-    partials[bid] = m;
-    partials[pstride + bid] = s;
+    const size_t gi = (row0 + rl) * N + pos;
+    const C* Ln = buf + rl * L::STRIDE;
+    const C a0 = Ln[fft_pad(pos)], a1 = Ln[fft_pad(pos + 1)], a2 = Ln[fft_pad(pos + 2)], a3 = Ln[fft_pad(pos + 3)];
+    if (re) *reinterpret_cast<float4*>(re + gi) = make_float4((float)a0.x, (float)a1.x, (float)a2.x, (float)a3.x);
+    if (im) *reinterpret_cast<float4*>(im + gi) = make_float4((float)a0.y, (float)a1.y, (float)a2.y, (float)a3.y);
   }
 }
 
-// Middle (y) pass of the 3D FFT, in place.  INV = false: natural in, paired out.
-// INV = true: paired in, natural out.  Tile: TXC complex columns x N rows at fixed z.
-template <int N, bool INV>
-__global__ void __launch_bounds__(kThreads) k_py(Geom g, int TXC, float2* __restrict__ Z) {
-  using C = LineCfg<N>;
-  extern __shared__ float2 smem[];
-  float2* buf = smem;
-  float2* tw = smem + C::LPB * C::STRIDE;
-  load_twiddles<N>(tw);
-  const int tilesx = g.nx / TXC;
-  const int x0 = (blockIdx.x % tilesx) * TXC;
-  const int z = blockIdx.x / tilesx;
-  float2* Zc = Z + blockIdx.y * g.F + ((size_t)z << (g.lx + g.ly)) + x0;
-  const int n = N * TXC;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int row = i / TXC, c = i % TXC;
-    const int q = INV ? paired_q(row, N) : row;
-    buf[c * C::STRIDE + fft_pad(q)] = Zc[(size_t)row * g.nx + c];
-  }
-  __syncthreads();
-  const int myline = threadIdx.x / C::T, tid = threadIdx.x % C::T;
-  fft_line<N, INV>(buf + myline * C::STRIDE, tw, tid, myline < TXC);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int row = i / TXC, c = i % TXC;
-    const int q = INV ? row : paired_q(row, N);
-    Zc[(size_t)row * g.nx + c] = buf[c * C::STRIDE + fft_pad(q)];
-  }
-}
-
-struct SpecParams {
-  float alpha;
+// Strided-axis pass (lines along y in 3D, along the last axis otherwise).  A tile is TXC
+// consecutive complex columns of NF fields (Leray: the d components together).
+//   MODE 0: forward FFT only        (3D y pass)
+//   MODE 1: inverse FFT only        (3D y^-1 pass)
+//   MODE 2: fwd, Z *= alpha L(k)/n, inv                     (v-chain last axis)
+//   MODE 3: fwd, Z *= -1/(alpha L~(k) n), inv               (b-chain last axis, no Leray)
+//   MODE 4: fwd, W_c = (P_L Z + i (-P_L Z / (alpha L~)))/n, inv   (b-chain, Leray, NF = d)
+struct SpecOp {
+  double alpha;
   int p;
-  int leray;
-  int ncomp;      // components processed per block (d if leray, else 1)
-  float invn;     // 1 / (nx ny nz)
+  double invn;
 };
 
-__device__ __forceinline__ float regL(float kk, int p) {
-  return p == 1 ? kk : (p == 2 ? kk * kk : kk * kk * kk);
-}
+__device__ __forceinline__ double regL(double kk, int p) { return p == 1 ? kk : (p == 2 ? kk * kk : kk * kk * kk); }
 
-// Fused last-axis pass: forward FFT along the last axis, spectral operator, inverse FFT.
-// 3D: tile = TXC x-positions (even) x 2 y-positions {2m, 2m+1} x N_z, for `ncomp` comps.
-// 2D: tile = TXC x-positions x N_y.
-// Spectral operator on each pair (k, -k):  v^ = (Z(k) + conj Z(-k))/2,
-// b^ = (Z(k) - conj Z(-k))/(2i), g^ = alpha L v^ + b^ (P_L g^ if leray),
-// s^ = -g^/(alpha L~), Z(k) <- (g^ + i s^)/n.  Partials: L|v^|^2, Re(s^ conj(L v^)), L|s^|^2.
-template <int N, int D>
-__global__ void __launch_bounds__(768) k_plast(Geom g, int TXC, SpecParams sp, float2* __restrict__ Z,
-                                               double* __restrict__ partials, int pstride) {
-  using C = LineCfg<N>;
-  extern __shared__ float2 smem[];
-  float2* tw = smem;
-  float2* buf = smem + N;
+template <int N, int MODE, typename C>
+__global__ void __launch_bounds__(kThreads) k_pstrided(Geom g, int axis, int TXC, int NF, ZList<C> Z, SpecOp op) {
+  using L = LineCfg<N>;
+  using T = typename Real<C>::T;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C* buf = reinterpret_cast<C*>(smraw);
+  C* tw = buf + NF * TXC * L::STRIDE;
   load_twiddles<N>(tw);
-  const int ny2 = D == 3 ? 2 : 1;                 // y-positions per tile
-  const int lines_per_comp = TXC * ny2;
-  const int nlines = lines_per_comp * sp.ncomp;
   const int tilesx = g.nx / TXC;
   const int x0 = (blockIdx.x % tilesx) * TXC;
-  const int y0 = D == 3 ? (blockIdx.x / tilesx) * 2 : 0;
-  const int comp0 = sp.ncomp == 1 ? blockIdx.y : 0;
-  const size_t S = D == 3 ? (size_t)g.nx * g.ny : (size_t)g.nx;  // stride along the last axis
-  // line l: comp = l / lines_per_comp, r = l % lines_per_comp, yy = r / TXC, c = r % TXC
-  auto gptr = [&](int l) -> float2* {
-    const int comp = comp0 + l / lines_per_comp, r = l % lines_per_comp;
-    const int yy = r / TXC, c = r % TXC;
-    return Z + comp * g.F + (size_t)(y0 + yy) * g.nx + x0 + c;
-  };
+  const int outer = blockIdx.x / tilesx;           // z (axis y) or y (axis z)
+  const int f0 = (MODE == 4) ? 0 : blockIdx.y;     // field of this block (Leray: all fields)
+  size_t base, S;
+  if (axis == 1) { base = ((size_t)outer << (g.lx + g.ly)) + x0; S = g.nx; }
+  else { base = ((size_t)outer << g.lx) + x0; S = (size_t)g.nx * g.ny; }
+  const int nlines = NF * TXC;
   const int n = N * nlines;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int row = i / nlines, l = i % nlines;
-    buf[l * C::STRIDE + fft_pad(row)] = gptr(l)[row * S];
+    const int f = f0 + l / TXC, c = l % TXC;
+    buf[l * L::STRIDE + fft_pad(row)] = Z.z[f][base + row * S + c];
   }
   __syncthreads();
-  const int myline = threadIdx.x / C::T, tid = threadIdx.x % C::T;
+  const int myline = threadIdx.x / L::T, tid = threadIdx.x % L::T;
   const bool active = myline < nlines;
-  fft_line<N, false>(buf + myline * C::STRIDE, tw, tid, active);
-
-  // spectral operator over points of one component-set: pt = (r, qz), r in [0, lines_per_comp)
-  double s_reg = 0.0, s_slv = 0.0, s_sls = 0.0;
-  const int npts = lines_per_comp * N;
-  const float al = sp.alpha;
-  for (int pt = threadIdx.x; pt < npts; pt += blockDim.x) {
-    const int r = pt / N, qz = pt % N;
-    const int yy = r / TXC, c = r % TXC;
-    const int xp = x0 + c, yp = y0 + yy;
-    // partner position
-    const int xpp = xp < 2 ? xp : (xp ^ 1);
-    const int ypp = D == 3 ? (yp < 2 ? yp : (yp ^ 1)) : 0;
-    const int qzp = (N - qz) & (N - 1);
-    const int rp = (ypp - y0) * TXC + (xpp - x0);
-    const int pt2 = rp * N + qzp;
-    if (pt2 < pt) continue;  // the partner's thread handles the pair
-    const bool self = pt2 == pt;
-    // wavenumbers (R2, R3)
-    const int qx = paired_q(xp, g.nx);
-    const float kx = kfreq(qx, g.nx), kpx = kprime(qx, g.nx);
-    float ky, kpy, kz, kpz;
-    if (D == 3) {
-      const int qy = paired_q(yp, g.ny);
-      ky = kfreq(qy, g.ny); kpy = kprime(qy, g.ny);
-      kz = kfreq(qz, N); kpz = kprime(qz, N);
-    } else {
-      ky = kfreq(qz, N); kpy = kprime(qz, N);
-      kz = 0.f; kpz = 0.f;
-    }
-    const float kk = kx * kx + ky * ky + kz * kz;
-    const float L = regL(kk, sp.p);
-    const float Lt = L == 0.f ? 1.f : L;  // kernel fix
-    float2 gh[3], vh[3];
-    for (int cc = 0; cc < sp.ncomp; ++cc) {
-      const float2 z1 = buf[(cc * lines_per_comp + r) * C::STRIDE + fft_pad(qz)];
-      const float2 z2 = buf[(cc * lines_per_comp + rp) * C::STRIDE + fft_pad(qzp)];
-      const float2 v1 = make_float2(0.5f * (z1.x + z2.x), 0.5f * (z1.y - z2.y));
-      // b^ = (z1 - conj z2) / (2i) = -i/2 (z1 - conj z2)
-      const float2 dd = make_float2(z1.x - z2.x, z1.y + z2.y);
-      const float2 b1 = make_float2(0.5f * dd.y, -0.5f * dd.x);
-      vh[cc] = v1;
-      gh[cc] = make_float2(fmaf(al * L, v1.x, b1.x), fmaf(al * L, v1.y, b1.y));
-    }
-    if (sp.leray) {
-      const float kp2 = kpx * kpx + kpy * kpy + kpz * kpz;
-      if (kp2 > 0.f) {
-        const float kp[3] = {kpx, kpy, kpz};
-        float2 dot = make_float2(0.f, 0.f);
-        for (int cc = 0; cc < sp.ncomp; ++cc) { dot.x += kp[cc] * gh[cc].x; dot.y += kp[cc] * gh[cc].y; }
-        const float inv = 1.0f / kp2;
-        for (int cc = 0; cc < sp.ncomp; ++cc) {
-          gh[cc].x -= kp[cc] * dot.x * inv;
-          gh[cc].y -= kp[cc] * dot.y * inv;
+  C* line = buf + myline * L::STRIDE;
+  if (MODE != 1) fft_line<N, false>(line, tw, tid, active);
+  if (MODE >= 2) {
+    // wavenumbers: x from the column, y from `outer` (3D, axis z) or the line position (2D)
+    for (int i = threadIdx.x; i < N * TXC; i += blockDim.x) {
+      const int q = i / TXC, c = i % TXC;
+      const int qx = x0 + c;
+      double kx = qx <= g.nx / 2 ? qx : qx - g.nx, kxp = qx == g.nx / 2 ? 0.0 : kx;
+      double ky, kyp, kz, kzp;
+      if (g.d == 3) {
+        const int qy = outer;
+        ky = qy <= g.ny / 2 ? qy : qy - g.ny; kyp = qy == g.ny / 2 ? 0.0 : ky;
+        kz = q <= N / 2 ? q : q - N; kzp = q == N / 2 ? 0.0 : kz;
+      } else {
+        ky = q <= N / 2 ? q : q - N; kyp = q == N / 2 ? 0.0 : ky;
+        kz = 0.0; kzp = 0.0;
+      }
+      const double Lk = regL(kx * kx + ky * ky + kz * kz, op.p);
+      if (MODE == 2 || MODE == 3) {
+        const double m = MODE == 2 ? op.alpha * Lk * op.invn : -op.invn / (op.alpha * (Lk == 0.0 ? 1.0 : Lk));
+        C& z = buf[c * L::STRIDE + fft_pad(q)];
+        z = mk((T)(z.x * m), (T)(z.y * m));
+      } else {
+        // Leray + inverse regulariser on the NF = d components at this k (R3, R9)
+        const double kp2 = kxp * kxp + kyp * kyp + kzp * kzp;
+        const double kp[3] = {kxp, kyp, kzp};
+        double bx[3], by[3];
+        for (int f = 0; f < NF; ++f) {
+          const C z = buf[(f * TXC + c) * L::STRIDE + fft_pad(q)];
+          bx[f] = z.x; by[f] = z.y;
+        }
+        if (kp2 > 0.0) {
+          double dx = 0.0, dy = 0.0;
+          for (int f = 0; f < NF; ++f) { dx += kp[f] * bx[f]; dy += kp[f] * by[f]; }
+          for (int f = 0; f < NF; ++f) { bx[f] -= kp[f] * dx / kp2; by[f] -= kp[f] * dy / kp2; }
+        }
+        const double ia = 1.0 / (op.alpha * (Lk == 0.0 ? 1.0 : Lk));
+        for (int f = 0; f < NF; ++f) {
+          // W = b_L^ + i p^,  p^ = -ia b_L^   =>  W = (bx + ia by) + i (by - ia bx)
+          buf[(f * TXC + c) * L::STRIDE + fft_pad(q)] =
+              mk((T)((bx[f] + ia * by[f]) * op.invn), (T)((by[f] - ia * bx[f]) * op.invn));
         }
       }
     }
-    const float invaL = 1.0f / (al * Lt);
-    const double mult = self ? 1.0 : 2.0;
-    for (int cc = 0; cc < sp.ncomp; ++cc) {
-      const float2 gg = gh[cc];
-      const float2 ss = make_float2(-gg.x * invaL, -gg.y * invaL);
-      const float2 vv = vh[cc];
-      s_reg += mult * (double)L * ((double)vv.x * vv.x + (double)vv.y * vv.y);
-      s_slv += mult * (double)L * ((double)ss.x * vv.x + (double)ss.y * vv.y);
-      s_sls += mult * (double)L * ((double)ss.x * ss.x + (double)ss.y * ss.y);
-      // W(k) = (g^ + i s^)/n ; W(-k) = (conj g^ + i conj s^)/n
-      const float in = sp.invn;
-      buf[(cc * lines_per_comp + r) * C::STRIDE + fft_pad(qz)] =
-          make_float2((gg.x - ss.y) * in, (gg.y + ss.x) * in);
-      if (!self)
-        buf[(cc * lines_per_comp + rp) * C::STRIDE + fft_pad(qzp)] =
-            make_float2((gg.x + ss.y) * in, (-gg.y + ss.x) * in);
-    }
+    __syncthreads();
   }
-  __syncthreads();
-  fft_line<N, true>(buf + myline * C::STRIDE, tw, tid, active);
+  if (MODE != 0) fft_line<N, true>(line, tw, tid, active);
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int row = i / nlines, l = i % nlines;
-    gptr(l)[row * S] = buf[l * C::STRIDE + fft_pad(row)];
+    const int f = f0 + l / TXC, c = l % TXC;
+    Z.z[f][base + row * S + c] = buf[l * L::STRIDE + fft_pad(row)];
   }
-  // partial sums
-  __shared__ double sh[3][32];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    s_reg += __shfl_down_sync(0xffffffffu, s_reg, o);
-    s_slv += __shfl_down_sync(0xffffffffu, s_slv, o);
-    s_sls += __shfl_down_sync(0xffffffffu, s_sls, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    sh[0][threadIdx.x >> 5] = s_reg; sh[1][threadIdx.x >> 5] = s_slv; sh[2][threadIdx.x >> 5] = s_sls;
+}
+
+// Assembly (x^-1 of the b-chain + pointwise combine), per x row (R9):
+//   g = u + b_L,  s = -(v - vbar) + p,  partial sums for the scalars.
+// Non-Leray: Z0 -> (p_x, p_y), Z1 -> (p_z, -), b_L = b.  Leray: Z_c -> (b_L,c, p_c).
+struct AsmArgs {
+  const float2* Z[3];
+  const float* b;      // d*F (non-Leray)
+  const float* u;      // d*F or null (0)
+  const float* v;      // d*F or null (0)
+  const double* vsum;  // device, d values (sum_x v_c); null => 0
+  float* g;            // d*F or null
+  float* s;            // d*F or null
+  double* partials;    // [10][kMaxPartials]
+};
+
+template <int N>
+__global__ void __launch_bounds__(kThreads) k_assemble(Geom g, int RB, int lpr, int leray, AsmArgs a) {
+  using L = LineCfg<N>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  float2* buf = reinterpret_cast<float2*>(smraw);
+  float2* tw = buf + RB * lpr * L::STRIDE;
+  load_twiddles<N>(tw);
+  const size_t nrows = (size_t)g.ny * g.nz;
+  const size_t row0 = (size_t)blockIdx.x * RB;
+  const int nlines = RB * lpr;
+  for (int i = threadIdx.x; i < nlines * N; i += blockDim.x) {
+    const int l = i / N, q = i % N;
+    const int r = l / lpr, f = l % lpr;
+    float2 z = make_float2(0.f, 0.f);
+    if (row0 + r < nrows) z = a.Z[f][(row0 + r) * N + q];
+    buf[l * L::STRIDE + fft_pad(q)] = z;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double a = 0, b = 0, c = 0;
-    for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) { a += sh[0][w]; b += sh[1][w]; c += sh[2][w]; }
-    const int bid = blockIdx.y * gridDim.x + blockIdx.x;
-    partials[bid] = a;
-    partials[pstride + bid] = b;
-    partials[2 * pstride + bid] = c;
+  const int myline = threadIdx.x / L::T, tid = threadIdx.x % L::T;
+  fft_line<N, true>(buf + myline * L::STRIDE, tw, tid, myline < nlines);
+  double gmax = 0.0, sgs = 0.0, svu = 0.0, ssu = 0.0, sg[3] = {0, 0, 0}, ss[3] = {0, 0, 0};
+  const double nF = (double)g.F;
+  for (int i = threadIdx.x; i < RB * N; i += blockDim.x) {
+    const int r = i / N, x = i % N;
+    if (row0 + r >= nrows) continue;
+    const size_t gi = (row0 + r) * N + x;
+    for (int c = 0; c < g.d; ++c) {
+      float bl, pc;
+      if (leray) {
+        const float2 w = buf[(r * lpr + c) * L::STRIDE + fft_pad(x)];
+        bl = w.x; pc = w.y;
+      } else {
+        const float2 w = buf[(r * lpr + c / 2) * L::STRIDE + fft_pad(x)];
+        pc = (c & 1) ? w.y : w.x;
+        bl = a.b ? a.b[c * g.F + gi] : 0.f;
+      }
+      const float uc = a.u ? a.u[c * g.F + gi] : 0.f;
+      const float vc = a.v ? a.v[c * g.F + gi] : 0.f;
+      const float vbar = a.vsum ? (float)(a.vsum[c] / nF) : 0.f;
+      const float gv = uc + bl;
+      const float sv = -(vc - vbar) + pc;
+      if (a.g) a.g[c * g.F + gi] = gv;
+      if (a.s) a.s[c * g.F + gi] = sv;
+      gmax = fmax(gmax, (double)fabsf(gv));
+      sgs += (double)gv * (double)sv;
+      svu += (double)vc * (double)uc;
+      ssu += (double)sv * (double)uc;
+      sg[c] += (double)gv;
+      ss[c] += (double)sv;
+    }
+  }
+  double vals[10] = {gmax, sgs, svu, ssu, sg[0], sg[1], sg[2], ss[0], ss[1], ss[2]};
+  __shared__ double sh[10][kThreads / 32];
+  const int nw = (blockDim.x + 31) / 32;
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+    double v = vals[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double w = __shfl_down_sync(0xffffffffu, v, o);
+      v = k == 0 ? fmax(v, w) : v + w;
+    }
+    if ((threadIdx.x & 31) == 0) sh[k][threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 10) {
+    const int k = threadIdx.x;
+    double acc = 0.0;
+    for (int w = 0; w < nw; ++w) acc = k == 0 ? fmax(acc, sh[k][w]) : acc + sh[k][w];
+    a.partials[(size_t)k * kMaxPartials + blockIdx.x] = acc;
   }
 }
 
-template <int N>
-static void px_fwd_dispatch(const Geom& g, const PrecondArgs& a, cudaStream_t st) {
-  using C = LineCfg<N>;
-  const size_t sm = line_smem<N>();
+template <int N, typename C>
+static size_t smem_lines(int nlines) {
+  return (size_t)(nlines * LineCfg<N>::STRIDE + N) * sizeof(C);
+}
+
+template <int N, typename C>
+static void px_fwd_launch(const Geom& g, const RealIn& in, const ZList<C>& Z, int nf, cudaStream_t st) {
+  using L = LineCfg<N>;
+  const size_t sm = smem_lines<N, C>(L::LPB);
   const size_t nrows = (size_t)g.ny * g.nz;
-  dim3 grid((unsigned)((nrows + C::LPB - 1) / C::LPB), g.d);
-  cudaFuncSetAttribute(k_px_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_px_fwd<N><<<grid, kThreads, sm, st>>>(g, a.v, a.b, a.Z);
+  dim3 grid((unsigned)((nrows + L::LPB - 1) / L::LPB), nf);
+  cudaFuncSetAttribute(k_px_fwd<N, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_px_fwd<N, C><<<grid, kThreads, sm, st>>>(g, in, Z);
 }
 
-template <int N>
-static void px_inv_dispatch(const Geom& g, const PrecondArgs& a, int* nparts, cudaStream_t st) {
-  using C = LineCfg<N>;
-  const size_t sm = line_smem<N>();
+template <int N, typename C>
+static void px_inv_launch(const Geom& g, const ZList<C>& Z, const RealOut& out, int nf, cudaStream_t st) {
+  using L = LineCfg<N>;
+  const size_t sm = smem_lines<N, C>(L::LPB);
   const size_t nrows = (size_t)g.ny * g.nz;
-  dim3 grid((unsigned)((nrows + C::LPB - 1) / C::LPB), g.d);
-  *nparts = grid.x * grid.y;
-  cudaFuncSetAttribute(k_px_inv<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_px_inv<N><<<grid, kThreads, sm, st>>>(g, a.Z, a.g, a.s, a.partials + 3 * kMaxPartials,
-                                          kMaxPartials);
+  dim3 grid((unsigned)((nrows + L::LPB - 1) / L::LPB), nf);
+  cudaFuncSetAttribute(k_px_inv<N, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_px_inv<N, C><<<grid, kThreads, sm, st>>>(g, Z, out);
 }
 
-template <int N>
-static void py_dispatch(const Geom& g, bool inv, const PrecondArgs& a, cudaStream_t st) {
-  using C = LineCfg<N>;
-  const size_t sm = line_smem<N>();
-  int TXC = C::LPB < g.nx ? C::LPB : g.nx;
-  dim3 grid((g.nx / TXC) * g.nz, g.d);
-  const int threads = TXC * C::T;
-  if (inv) {
-    cudaFuncSetAttribute(k_py<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_py<N, true><<<grid, threads, sm, st>>>(g, TXC, a.Z);
-  } else {
-    cudaFuncSetAttribute(k_py<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_py<N, false><<<grid, threads, sm, st>>>(g, TXC, a.Z);
-  }
-}
-
-template <int N>
-static void plast_dispatch(const Geom& g, const PrecondArgs& a, int* nparts, cudaStream_t st) {
-  using C = LineCfg<N>;
-  SpecParams sp;
-  sp.alpha = (float)a.alpha;
-  sp.p = a.p;
-  sp.leray = a.leray ? 1 : 0;
-  sp.ncomp = a.leray ? g.d : 1;
-  sp.invn = (float)(1.0 / ((double)g.nx * g.ny * g.nz));
-  const int ny2 = g.d == 3 ? 2 : 1;
-  // lines per block target ~ LPB (256 threads); at least 2 x-positions per tile
-  int TXC = C::LPB / (ny2 * sp.ncomp);
-  int t = 2;
+template <int N, int MODE, typename C>
+static void pstrided_launch(const Geom& g, int axis, const ZList<C>& Z, int nf, const SpecOp& op, cudaStream_t st) {
+  using L = LineCfg<N>;
+  const int NF = MODE == 4 ? nf : 1;
+  int TXC = L::LPB / NF;
+  int t = 1;
   while (t * 2 <= TXC) t *= 2;
-  TXC = t < 2 ? 2 : t;
+  TXC = t;
   if (TXC > g.nx) TXC = g.nx;
-  const int nlines = TXC * ny2 * sp.ncomp;
-  const int threads = nlines * C::T;
-  const size_t sm = (size_t)(N + nlines * C::STRIDE) * sizeof(float2);
-  const int tiles = (g.nx / TXC) * (g.d == 3 ? g.ny / 2 : 1);
-  dim3 grid(tiles, sp.ncomp == 1 ? g.d : 1);
-  *nparts = grid.x * grid.y;
-  double* part = a.partials;
-  if (g.d == 3) {
-    cudaFuncSetAttribute(k_plast<N, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_plast<N, 3><<<grid, threads, sm, st>>>(g, TXC, sp, a.Z, part, kMaxPartials);
-  } else {
-    cudaFuncSetAttribute(k_plast<N, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_plast<N, 2><<<grid, threads, sm, st>>>(g, TXC, sp, a.Z, part, kMaxPartials);
-  }
+  if (TXC < 1) TXC = 1;
+  const size_t sm = smem_lines<N, C>(NF * TXC);
+  const int outer = axis == 1 ? g.nz : g.ny;
+  dim3 grid((g.nx / TXC) * outer, MODE == 4 ? 1 : nf);
+  const int threads = NF * TXC * L::T;
+  cudaFuncSetAttribute(k_pstrided<N, MODE, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_pstrided<N, MODE, C><<<grid, threads, sm, st>>>(g, axis, TXC, NF, Z, op);
 }
 
-// Full preconditioner: 3D: x, y, [z fused], y^-1, x^-1;  2D: x, [y fused], x^-1.
-// Scalars written: REG, SLV, SLS (spectral, h^d/n weighted), GRAD_INF, GS (real space).
-void launch_precond(const Geom& g, const PrecondArgs& a, cudaStream_t st) {
-  TOPT_DISPATCH_N(g.nx, px_fwd_dispatch, g, a, st);
-  if (g.d == 3) TOPT_DISPATCH_N(g.ny, py_dispatch, g, false, a, st);
-  int np_last = 0, np_inv = 0;
-  const int Nl = g.d == 3 ? g.nz : g.ny;
-  TOPT_DISPATCH_N(Nl, plast_dispatch, g, a, &np_last, st);
-  if (g.d == 3) TOPT_DISPATCH_N(g.ny, py_dispatch, g, true, a, st);
-  TOPT_DISPATCH_N(g.nx, px_inv_dispatch, g, a, &np_inv, st);
-  if (a.scalars) {
-    const double n = (double)g.F;
-    const double sc = a.cellvol / n;  // Parseval: <a,b>_h = h^d/n sum_k a^ conj b^
-    launch_finalize(a.partials, 0, np_last, 0.5 * a.alpha * sc, false, a.scalars + TOPT_S_REG, st);
-    launch_finalize(a.partials, 1, np_last, a.alpha * sc, false, a.scalars + TOPT_S_SLV, st);
-    launch_finalize(a.partials, 2, np_last, a.alpha * sc, false, a.scalars + TOPT_S_SLS, st);
-    launch_finalize(a.partials, 3, np_inv, 1.0, true, a.scalars + TOPT_S_GRAD_INF, st);
-    launch_finalize(a.partials, 4, np_inv, a.cellvol, false, a.scalars + TOPT_S_GS, st);
+template <int N, int MODE, typename C>
+static void pstrided_dispatch_helper(const Geom& g, int axis, const ZList<C>& Z, int nf, const SpecOp& op,
+                                     cudaStream_t st) {
+  pstrided_launch<N, MODE, C>(g, axis, Z, nf, op, st);
+}
+
+#define TOPT_DISPATCH_N2(NV, BODY)                                  \
+  switch (NV) {                                                     \
+    case 8: { constexpr int N_ = 8; BODY; } break;                  \
+    case 16: { constexpr int N_ = 16; BODY; } break;                \
+    case 32: { constexpr int N_ = 32; BODY; } break;                \
+    case 64: { constexpr int N_ = 64; BODY; } break;                \
+    case 128: { constexpr int N_ = 128; BODY; } break;              \
+    case 256: { constexpr int N_ = 256; BODY; } break;              \
+    case 512: { constexpr int N_ = 512; BODY; } break;              \
+    case 1024: { constexpr int N_ = 1024; BODY; } break;            \
+    default: fprintf(stderr, "topt: unsupported N %d\n", NV);       \
   }
+
+// u = alpha L v with fp64 arithmetic and fp64 intermediates (Zv: 2 double2 fields of F).
+void launch_vchain(const Geom& g, const float* v, double2* Zv, float* u, double alpha, int p, cudaStream_t st) {
+  const int nf = g.d == 3 ? 2 : 1;
+  ZList<double2> Z{{Zv, Zv + g.F, nullptr}};
+  RealIn in{{v, g.d == 3 ? v + 2 * g.F : nullptr, nullptr}, {v + g.F, nullptr, nullptr}};
+  SpecOp op{alpha, p, 1.0 / (double)g.F};
+  TOPT_DISPATCH_N2(g.nx, (px_fwd_launch<N_, double2>(g, in, Z, nf, st)));
+  if (g.d == 3) {
+    TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 0, double2>(g, 1, Z, nf, op, st)));
+    TOPT_DISPATCH_N2(g.nz, (pstrided_launch<N_, 2, double2>(g, 2, Z, nf, op, st)));
+    TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 1, double2>(g, 1, Z, nf, op, st)));
+  } else {
+    TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 2, double2>(g, 1, Z, nf, op, st)));
+  }
+  RealOut out{{u, g.d == 3 ? u + 2 * g.F : nullptr, nullptr}, {u + g.F, nullptr, nullptr}};
+  TOPT_DISPATCH_N2(g.nx, (px_inv_launch<N_, double2>(g, Z, out, nf, st)));
+}
+
+// b-chain up to (not including) the x^-1 pass, which the assembly kernel performs.
+void launch_bchain(const Geom& g, const float* b, float2* Zb, double alpha, int p, bool leray, cudaStream_t st) {
+  const size_t F = g.F;
+  SpecOp op{alpha, p, 1.0 / (double)F};
+  ZList<float2> Z{{Zb, Zb + F, Zb + 2 * F}};
+  int nf;
+  RealIn in{};
+  if (leray) {
+    nf = g.d;
+    for (int c = 0; c < g.d; ++c) { in.re[c] = b + c * F; in.im[c] = nullptr; }
+  } else {
+    nf = g.d == 3 ? 2 : 1;
+    in.re[0] = b; in.im[0] = b + F;
+    if (g.d == 3) { in.re[1] = b + 2 * F; in.im[1] = nullptr; }
+  }
+  TOPT_DISPATCH_N2(g.nx, (px_fwd_launch<N_, float2>(g, in, Z, nf, st)));
+  const int last_axis = g.d == 3 ? 2 : 1;
+  const int Nl = g.d == 3 ? g.nz : g.ny;
+  if (g.d == 3) TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 0, float2>(g, 1, Z, nf, op, st)));
+  if (leray) {
+    TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 4, float2>(g, last_axis, Z, nf, op, st)));
+  } else {
+    TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 3, float2>(g, last_axis, Z, nf, op, st)));
+  }
+  if (g.d == 3) TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 1, float2>(g, 1, Z, nf, op, st)));
+}
+
+template <int N>
+static void assemble_launch(const Geom& g, bool leray, const AsmArgs& a, int* nparts, cudaStream_t st) {
+  using L = LineCfg<N>;
+  const int lpr = leray ? g.d : (g.d == 3 ? 2 : 1);
+  int RB = L::LPB / lpr;
+  if (RB < 1) RB = 1;
+  const size_t sm = smem_lines<N, float2>(RB * lpr);
+  const size_t nrows = (size_t)g.ny * g.nz;
+  const int blocks = (int)((nrows + RB - 1) / RB);
+  *nparts = blocks;
+  cudaFuncSetAttribute(k_assemble<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_assemble<N><<<blocks, RB * lpr * L::T, sm, st>>>(g, RB, lpr, leray ? 1 : 0, a);
+}
+
+void launch_assemble(const Geom& g, const float2* Zb, bool leray, const float* b, const float* u, const float* v,
+                     const double* vsum, float* gout, float* sout, double* partials, int* nparts, cudaStream_t st) {
+  const size_t F = g.F;
+  AsmArgs a{{Zb, Zb + F, Zb + 2 * F}, b, u, v, vsum, gout, sout, partials};
+  TOPT_DISPATCH_N2(g.nx, (assemble_launch<N_>(g, leray, a, nparts, st)));
 }
 
 }  // namespace topt
