@@ -56,6 +56,7 @@ class LineSearchState:
     trials: int = 0
     stagnated: bool = False
     replay: list = field(default_factory=list)  # optional forced rho sequence (debug)
+    accepted: list = field(default_factory=list)  # accepted rho per q evaluation (for replay)
 
 
 class TransportFP:
@@ -85,6 +86,7 @@ class TransportFP:
         if ls.replay:
             rho = ls.replay.pop(0)
             ls.rho = rho
+            ls.accepted.append(rho)
             return v + rho * s
         rho = ls.rho
         for t in range(ls.max_backtracks + 1):
@@ -92,6 +94,7 @@ class TransportFP:
             ls.trials += 1
             if self.objective(vt) < obj0 + rho * ls.c * gs:
                 ls.rho = 2.0 * rho if t == 0 else rho
+                ls.accepted.append(rho)
                 return vt
             rho *= 0.5
         ls.stagnated = True
@@ -246,5 +249,6 @@ def solve(prob: _gradient.Problem, w, sigma=1, tau=0, n_iter=200, eps_rel=5e-2,
     res = run(fp, v0, w, sigma, tau, n_iter, eps_rel, ordering, ls)
     res.info = dict(res.info)
     res.info.update(grad_evals=fp.grad_evals, obj_evals=fp.obj_evals,
-                    pde_solves=fp.pde_solves(), rho=ls.rho, trials=ls.trials)
+                    pde_solves=fp.pde_solves(), rho=ls.rho, trials=ls.trials,
+                    accepted=list(ls.accepted))
     return res

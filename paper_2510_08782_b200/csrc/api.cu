@@ -63,8 +63,8 @@ struct topt_ctx {
   char* ws = nullptr;
   size_t ws_bytes = 0, ws_need = 0;
   float *m_traj{}, *lam_traj{}, *df{}, *da{}, *E{}, *divv{}, *b{}, *utmp{};
-  float2* Z{};      // b-chain: 3 complex fields of F
-  double2* Zv{};    // v-chain: 2 double-complex fields of F
+  float2* Z{};      // b-chain: 4 complex fields of F
+  double2* Zv{};    // v-chain: 3 double-complex fields of F
   float *m0b{}, *m1b{}, *vb{}, *vt{};
   float *vcur{}, *gcur{}, *scur{}, *q{}, *gq{}, *sq{}, *vnew{}, *gnew{}, *snew{};
   float *ucur{}, *uq{}, *unew{};  // u = alpha L v tracked alongside v
@@ -178,8 +178,8 @@ topt_status topt_create(const topt_params* p, int32_t rank, int32_t world, const
   add(F * 4); add(F * 4); // E, divv
   add(V * 4);             // b
   add(V * 4);             // utmp
-  add(3 * F * 8);         // Z (3 complex fields)
-  add(2 * F * 16);        // Zv (2 double-complex fields)
+  add(4 * F * 8);         // Z (4 complex fields)
+  add(3 * F * 16);        // Zv (3 double-complex fields)
   add(F * 4); add(F * 4); add(V * 4); add(V * 4);  // m0b, m1b, vb, vt
   for (int i = 0; i < 12; ++i) add(V * 4);         // vcur..snew, ucur, uq, unew
   add(3 * W1 * V * 4);    // history
@@ -229,8 +229,8 @@ topt_status topt_bind_workspace(topt_ctx* c, void* dptr, size_t bytes) {
   c->divv = (float*)take(F * 4);
   c->b = (float*)take(V * 4);
   c->utmp = (float*)take(V * 4);
-  c->Z = (float2*)take(3 * F * 8);
-  c->Zv = (double2*)take(2 * F * 16);
+  c->Z = (float2*)take(4 * F * 8);
+  c->Zv = (double2*)take(3 * F * 16);
   c->m0b = (float*)take(F * 4);
   c->m1b = (float*)take(F * 4);
   c->vb = (float*)take(V * 4);
@@ -330,7 +330,7 @@ void backward_half(topt_ctx* c, const float* v, const float* u, float* gout, flo
     launch_deriv_accum(g, a, da, st);
   }
   if (!u) {
-    launch_vchain(g, v, c->Zv, c->utmp, c->p.alpha, c->p.reg_order, st);
+    launch_vchain(g, v, c->Zv, c->utmp, c->p.alpha, c->p.reg_order, c->p.model == TOPT_INCOMPRESSIBLE, st);
     u = c->utmp;
   }
   const bool leray = c->p.model == TOPT_INCOMPRESSIBLE;
@@ -497,7 +497,7 @@ topt_status topt_objective(topt_ctx* c, const float* m0, const float* m1, const 
   cudaStream_t st = (cudaStream_t)stream;
   forward_half(c, m0, m1, v, false, d_scalars, intl(c, 4), st);
   // reg = alpha/2 <v, L v>_h = h^d/2 sum v u,  u = alpha L v (fp64 chain)
-  launch_vchain(c->g, v, c->Zv, c->utmp, c->p.alpha, c->p.reg_order, st);
+  launch_vchain(c->g, v, c->Zv, c->utmp, c->p.alpha, c->p.reg_order, false, st);  // plain L, as in (1.1a)
   const float* bs[1] = {c->utmp};
   int np = 0;
   launch_multidot(v, bs, 1, c->vecN, c->partials, &np, st);
@@ -662,7 +662,7 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
   // v^0, u^0 = alpha L v^0 (fp64 chain, once), g(v^0)
   TOPT_CUDA(cudaMemcpyAsync(c->vcur, v_inout, V * 4, cudaMemcpyDeviceToDevice, st));
   if (leray) leray_inplace(c, c->vcur, st);
-  launch_vchain(c->g, c->vcur, c->Zv, c->ucur, P.alpha, P.reg_order, st);
+  launch_vchain(c->g, c->vcur, c->Zv, c->ucur, P.alpha, P.reg_order, leray, st);
   double te = now();
   if ((r = eval_gradient(c, m0, m1, c->vcur, c->ucur, c->gcur, c->scur, pub(c, 0), intl(c, 0), st)) != TOPT_OK)
     return r;

@@ -66,9 +66,10 @@ struct DerivArgs {
 };
 void launch_deriv_accum(const Geom& g, int axis, const DerivArgs& a, cudaStream_t st);
 
-// u = alpha L v (fp64 chain; Zv = 2 double2 fields of F)
-void launch_vchain(const Geom& g, const float* v, double2* Zv, float* u, double alpha, int p, cudaStream_t st);
-// b-chain up to the x^-1 pass (Zb = 3 float2 fields of F); see kernels_spectral.cu
+// u = alpha L v (alpha L P_L v if leray); fp64 chain, Zv = 3 double2 fields of F
+void launch_vchain(const Geom& g, const float* v, double2* Zv, float* u, double alpha, int p, bool leray,
+                   cudaStream_t st);
+// b-chain up to the x^-1 pass (Zb = 4 float2 fields of F); see kernels_spectral.cu
 void launch_bchain(const Geom& g, const float* b, float2* Zb, double alpha, int p, bool leray, cudaStream_t st);
 // x^-1 of the b-chain and pointwise assembly g = u + b_L, s = -(v - vbar) + p, with
 // partial sums in slots 0..9 (max|g|, sum gs, sum vu, sum su, sum g_c (3), sum s_c (3)).

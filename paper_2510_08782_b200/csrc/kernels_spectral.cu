@@ -291,11 +291,14 @@ void launch_deriv_accum(const Geom& g, int axis, const DerivArgs& a, cudaStream_
 //    alpha L(k) is real and even.
 //  b-chain (fp32): the smoothing inverse -(alpha L~)^{-1} and the Leray projector are
 //    well conditioned.  Non-Leray: Z0 = b_x + i b_y, Z1 = b_z -> W = -Z/(alpha L~ n) gives
-//    p = -(alpha L~)^{-1} b.  Leray: Z_c = b_c (real) -> W_c = (P_L b^ + i p^)/n with
-//    p^ = -P_L b^ / (alpha L~) (pointwise in k across components, R3/R9).
+//    p = -(alpha L~)^{-1} b.  Leray (R3, R9): Z_c = b_c (real, c < d); at each k the
+//    projected b_L^ = P_L b^ and p^ = -b_L^/(alpha L~) are written as separate pairs
+//    (b_Lx + i b_Ly), (b_Lz), (p_x + i p_y), (p_z) — never b_L and p in one complex field,
+//    whose magnitudes differ by up to 1/alpha and would pollute each other in fp32.
+//  Incompressible v-chain: Z_c = v_c (fp64) -> (u_x + i u_y), (u_z), u = alpha L P_L v.
 // =====================================================================================
 template <typename C>
-struct ZList { C* z[3]; };
+struct ZList { C* z[4]; };
 struct RealIn { const float* re[3]; const float* im[3]; };
 
 // x pass forward: Z_f[row][q] = FFT_x(re_f + i im_f)[q]
@@ -374,12 +377,14 @@ __global__ void __launch_bounds__(kThreads) k_px_inv(Geom g, ZList<C> Z, RealOut
 }
 
 // Strided-axis pass (lines along y in 3D, along the last axis otherwise).  A tile is TXC
-// consecutive complex columns of NF fields (Leray: the d components together).
+// consecutive complex columns of NIN fields (Leray modes: the d components together),
+// written back as NOUT fields.
 //   MODE 0: forward FFT only        (3D y pass)
 //   MODE 1: inverse FFT only        (3D y^-1 pass)
-//   MODE 2: fwd, Z *= alpha L(k)/n, inv                     (v-chain last axis)
-//   MODE 3: fwd, Z *= -1/(alpha L~(k) n), inv               (b-chain last axis, no Leray)
-//   MODE 4: fwd, W_c = (P_L Z + i (-P_L Z / (alpha L~)))/n, inv   (b-chain, Leray, NF = d)
+//   MODE 2: fwd, Z *= alpha L(k)/n, inv                        (v-chain, last axis)
+//   MODE 3: fwd, Z *= -1/(alpha L~(k) n), inv                  (b-chain, last axis)
+//   MODE 4: fwd, Leray + inverse regulariser, inv; d -> 2 (2D) / 4 (3D) fields (b-chain)
+//   MODE 5: fwd, alpha L P_L, inv; d -> 1 (2D) / 2 (3D) fields (incompressible v-chain)
 struct SpecOp {
   double alpha;
   int p;
@@ -389,38 +394,36 @@ struct SpecOp {
 __device__ __forceinline__ double regL(double kk, int p) { return p == 1 ? kk : (p == 2 ? kk * kk : kk * kk * kk); }
 
 template <int N, int MODE, typename C>
-__global__ void __launch_bounds__(kThreads) k_pstrided(Geom g, int axis, int TXC, int NF, ZList<C> Z, SpecOp op) {
+__global__ void __launch_bounds__(kThreads) k_pstrided(Geom g, int axis, int TXC, int NIN, int NOUT, ZList<C> Z,
+                                                       SpecOp op) {
   using L = LineCfg<N>;
   using T = typename Real<C>::T;
   extern __shared__ __align__(16) unsigned char smraw[];
   C* buf = reinterpret_cast<C*>(smraw);
-  C* tw = buf + NF * TXC * L::STRIDE;
+  const int NL = NIN > NOUT ? NIN : NOUT;  // line slots per column
+  C* tw = buf + NL * TXC * L::STRIDE;
   load_twiddles<N>(tw);
   const int tilesx = g.nx / TXC;
   const int x0 = (blockIdx.x % tilesx) * TXC;
   const int outer = blockIdx.x / tilesx;           // z (axis y) or y (axis z)
-  const int f0 = (MODE == 4) ? 0 : blockIdx.y;     // field of this block (Leray: all fields)
+  const int f0 = (MODE >= 4) ? 0 : blockIdx.y;     // field of this block (Leray modes: all fields)
   size_t base, S;
   if (axis == 1) { base = ((size_t)outer << (g.lx + g.ly)) + x0; S = g.nx; }
   else { base = ((size_t)outer << g.lx) + x0; S = (size_t)g.nx * g.ny; }
-  const int nlines = NF * TXC;
-  const int n = N * nlines;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int row = i / nlines, l = i % nlines;
+  const int nin = NIN * TXC;
+  for (int i = threadIdx.x; i < N * nin; i += blockDim.x) {
+    const int row = i / nin, l = i % nin;
     const int f = f0 + l / TXC, c = l % TXC;
     buf[l * L::STRIDE + fft_pad(row)] = Z.z[f][base + row * S + c];
   }
   __syncthreads();
   const int myline = threadIdx.x / L::T, tid = threadIdx.x % L::T;
-  const bool active = myline < nlines;
-  C* line = buf + myline * L::STRIDE;
-  if (MODE != 1) fft_line<N, false>(line, tw, tid, active);
+  if (MODE != 1) fft_line<N, false>(buf + myline * L::STRIDE, tw, tid, myline < nin);
   if (MODE >= 2) {
-    // wavenumbers: x from the column, y from `outer` (3D, axis z) or the line position (2D)
     for (int i = threadIdx.x; i < N * TXC; i += blockDim.x) {
       const int q = i / TXC, c = i % TXC;
       const int qx = x0 + c;
-      double kx = qx <= g.nx / 2 ? qx : qx - g.nx, kxp = qx == g.nx / 2 ? 0.0 : kx;
+      const double kx = qx <= g.nx / 2 ? qx : qx - g.nx, kxp = qx == g.nx / 2 ? 0.0 : kx;
       double ky, kyp, kz, kzp;
       if (g.d == 3) {
         const int qy = outer;
@@ -431,37 +434,50 @@ __global__ void __launch_bounds__(kThreads) k_pstrided(Geom g, int axis, int TXC
         kz = 0.0; kzp = 0.0;
       }
       const double Lk = regL(kx * kx + ky * ky + kz * kz, op.p);
+      const double Lt = Lk == 0.0 ? 1.0 : Lk;  // kernel fix
       if (MODE == 2 || MODE == 3) {
-        const double m = MODE == 2 ? op.alpha * Lk * op.invn : -op.invn / (op.alpha * (Lk == 0.0 ? 1.0 : Lk));
+        const double m = MODE == 2 ? op.alpha * Lk * op.invn : -op.invn / (op.alpha * Lt);
         C& z = buf[c * L::STRIDE + fft_pad(q)];
         z = mk((T)(z.x * m), (T)(z.y * m));
       } else {
-        // Leray + inverse regulariser on the NF = d components at this k (R3, R9)
+        // Leray on the d components at this k (Nyquist-zeroed k', R3/R9)
         const double kp2 = kxp * kxp + kyp * kyp + kzp * kzp;
         const double kp[3] = {kxp, kyp, kzp};
-        double bx[3], by[3];
-        for (int f = 0; f < NF; ++f) {
+        double bx[3] = {0, 0, 0}, by[3] = {0, 0, 0};
+        for (int f = 0; f < NIN; ++f) {
           const C z = buf[(f * TXC + c) * L::STRIDE + fft_pad(q)];
           bx[f] = z.x; by[f] = z.y;
         }
         if (kp2 > 0.0) {
           double dx = 0.0, dy = 0.0;
-          for (int f = 0; f < NF; ++f) { dx += kp[f] * bx[f]; dy += kp[f] * by[f]; }
-          for (int f = 0; f < NF; ++f) { bx[f] -= kp[f] * dx / kp2; by[f] -= kp[f] * dy / kp2; }
+          for (int f = 0; f < NIN; ++f) { dx += kp[f] * bx[f]; dy += kp[f] * by[f]; }
+          for (int f = 0; f < NIN; ++f) { bx[f] -= kp[f] * dx / kp2; by[f] -= kp[f] * dy / kp2; }
         }
-        const double ia = 1.0 / (op.alpha * (Lk == 0.0 ? 1.0 : Lk));
-        for (int f = 0; f < NF; ++f) {
-          // W = b_L^ + i p^,  p^ = -ia b_L^   =>  W = (bx + ia by) + i (by - ia bx)
-          buf[(f * TXC + c) * L::STRIDE + fft_pad(q)] =
-              mk((T)((bx[f] + ia * by[f]) * op.invn), (T)((by[f] - ia * bx[f]) * op.invn));
+        // each component's spectrum is bx + i by; pack pairs of REAL fields: A + i B has
+        // spectrum A^ + i B^ = (Ax - By) + i (Ay + Bx)
+        const double sl = MODE == 5 ? op.alpha * Lk * op.invn : op.invn;
+        const double sp = -op.invn / (op.alpha * Lt);
+        auto put = [&](int slot, int a, int b, double sa, double sb) {
+          const double ax = a >= 0 ? sa * bx[a] : 0.0, ay = a >= 0 ? sa * by[a] : 0.0;
+          const double cx = b >= 0 ? sb * bx[b] : 0.0, cy = b >= 0 ? sb * by[b] : 0.0;
+          buf[(slot * TXC + c) * L::STRIDE + fft_pad(q)] = mk((T)(ax - cy), (T)(ay + cx));
+        };
+        if (g.d == 3) {
+          put(0, 0, 1, sl, sl);
+          put(1, 2, -1, sl, 0.0);
+          if (MODE == 4) { put(2, 0, 1, sp, sp); put(3, 2, -1, sp, 0.0); }
+        } else {
+          put(0, 0, 1, sl, sl);
+          if (MODE == 4) put(1, 0, 1, sp, sp);
         }
       }
     }
     __syncthreads();
   }
-  if (MODE != 0) fft_line<N, true>(line, tw, tid, active);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int row = i / nlines, l = i % nlines;
+  const int nout = NOUT * TXC;
+  if (MODE != 0) fft_line<N, true>(buf + myline * L::STRIDE, tw, tid, myline < nout);
+  for (int i = threadIdx.x; i < N * nout; i += blockDim.x) {
+    const int row = i / nout, l = i % nout;
     const int f = f0 + l / TXC, c = l % TXC;
     Z.z[f][base + row * S + c] = buf[l * L::STRIDE + fft_pad(row)];
   }
@@ -469,9 +485,10 @@ __global__ void __launch_bounds__(kThreads) k_pstrided(Geom g, int axis, int TXC
 
 // Assembly (x^-1 of the b-chain + pointwise combine), per x row (R9):
 //   g = u + b_L,  s = -(v - vbar) + p,  partial sums for the scalars.
-// Non-Leray: Z0 -> (p_x, p_y), Z1 -> (p_z, -), b_L = b.  Leray: Z_c -> (b_L,c, p_c).
+// Fields per row: non-Leray (p_x + i p_y)[, (p_z)], b_L = b from memory;
+//                 Leray (b_Lx + i b_Ly)[, (b_Lz)], (p_x + i p_y)[, (p_z)].
 struct AsmArgs {
-  const float2* Z[3];
+  const float2* Z[4];
   const float* b;      // d*F (non-Leray)
   const float* u;      // d*F or null (0)
   const float* v;      // d*F or null (0)
@@ -507,14 +524,15 @@ __global__ void __launch_bounds__(kThreads) k_assemble(Geom g, int RB, int lpr, 
     const int r = i / N, x = i % N;
     if (row0 + r >= nrows) continue;
     const size_t gi = (row0 + r) * N + x;
+    const int pf = leray ? lpr / 2 : 0;  // first p field
     for (int c = 0; c < g.d; ++c) {
       float bl, pc;
+      const float2 wp = buf[(r * lpr + pf + c / 2) * L::STRIDE + fft_pad(x)];
+      pc = (c & 1) ? wp.y : wp.x;
       if (leray) {
-        const float2 w = buf[(r * lpr + c) * L::STRIDE + fft_pad(x)];
-        bl = w.x; pc = w.y;
+        const float2 wb = buf[(r * lpr + c / 2) * L::STRIDE + fft_pad(x)];
+        bl = (c & 1) ? wb.y : wb.x;
       } else {
-        const float2 w = buf[(r * lpr + c / 2) * L::STRIDE + fft_pad(x)];
-        pc = (c & 1) ? w.y : w.x;
         bl = a.b ? a.b[c * g.F + gi] : 0.f;
       }
       const float uc = a.u ? a.u[c * g.F + gi] : 0.f;
@@ -580,27 +598,24 @@ static void px_inv_launch(const Geom& g, const ZList<C>& Z, const RealOut& out, 
 }
 
 template <int N, int MODE, typename C>
-static void pstrided_launch(const Geom& g, int axis, const ZList<C>& Z, int nf, const SpecOp& op, cudaStream_t st) {
+static void pstrided_launch(const Geom& g, int axis, const ZList<C>& Z, int nin, int nout, const SpecOp& op,
+                            cudaStream_t st) {
   using L = LineCfg<N>;
-  const int NF = MODE == 4 ? nf : 1;
-  int TXC = L::LPB / NF;
+  const bool multi = MODE >= 4;
+  const int NIN = multi ? nin : 1, NOUT = multi ? nout : 1;
+  const int NL = NIN > NOUT ? NIN : NOUT;
+  int TXC = L::LPB / NL;
   int t = 1;
   while (t * 2 <= TXC) t *= 2;
   TXC = t;
   if (TXC > g.nx) TXC = g.nx;
   if (TXC < 1) TXC = 1;
-  const size_t sm = smem_lines<N, C>(NF * TXC);
+  const size_t sm = smem_lines<N, C>(NL * TXC);
   const int outer = axis == 1 ? g.nz : g.ny;
-  dim3 grid((g.nx / TXC) * outer, MODE == 4 ? 1 : nf);
-  const int threads = NF * TXC * L::T;
+  dim3 grid((g.nx / TXC) * outer, multi ? 1 : nin);
+  const int threads = NL * TXC * L::T;
   cudaFuncSetAttribute(k_pstrided<N, MODE, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_pstrided<N, MODE, C><<<grid, threads, sm, st>>>(g, axis, TXC, NF, Z, op);
-}
-
-template <int N, int MODE, typename C>
-static void pstrided_dispatch_helper(const Geom& g, int axis, const ZList<C>& Z, int nf, const SpecOp& op,
-                                     cudaStream_t st) {
-  pstrided_launch<N, MODE, C>(g, axis, Z, nf, op, st);
+  k_pstrided<N, MODE, C><<<grid, threads, sm, st>>>(g, axis, TXC, NIN, NOUT, Z, op);
 }
 
 #define TOPT_DISPATCH_N2(NV, BODY)                                  \
@@ -616,55 +631,65 @@ static void pstrided_dispatch_helper(const Geom& g, int axis, const ZList<C>& Z,
     default: fprintf(stderr, "topt: unsupported N %d\n", NV);       \
   }
 
-// u = alpha L v with fp64 arithmetic and fp64 intermediates (Zv: 2 double2 fields of F).
-void launch_vchain(const Geom& g, const float* v, double2* Zv, float* u, double alpha, int p, cudaStream_t st) {
-  const int nf = g.d == 3 ? 2 : 1;
-  ZList<double2> Z{{Zv, Zv + g.F, nullptr}};
-  RealIn in{{v, g.d == 3 ? v + 2 * g.F : nullptr, nullptr}, {v + g.F, nullptr, nullptr}};
-  SpecOp op{alpha, p, 1.0 / (double)g.F};
-  TOPT_DISPATCH_N2(g.nx, (px_fwd_launch<N_, double2>(g, in, Z, nf, st)));
-  if (g.d == 3) {
-    TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 0, double2>(g, 1, Z, nf, op, st)));
-    TOPT_DISPATCH_N2(g.nz, (pstrided_launch<N_, 2, double2>(g, 2, Z, nf, op, st)));
-    TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 1, double2>(g, 1, Z, nf, op, st)));
+// u = alpha L v (P_L first if leray) with fp64 arithmetic and fp64 intermediates.
+// Zv: 3 double2 fields of F.
+void launch_vchain(const Geom& g, const float* v, double2* Zv, float* u, double alpha, int p, bool leray,
+                   cudaStream_t st) {
+  const size_t F = g.F;
+  ZList<double2> Z{{Zv, Zv + F, Zv + 2 * F, nullptr}};
+  SpecOp op{alpha, p, 1.0 / (double)F};
+  RealIn in{};
+  int nin, nout = g.d == 3 ? 2 : 1;
+  if (leray) {
+    nin = g.d;
+    for (int c = 0; c < g.d; ++c) { in.re[c] = v + c * F; in.im[c] = nullptr; }
   } else {
-    TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 2, double2>(g, 1, Z, nf, op, st)));
+    nin = nout;
+    in.re[0] = v; in.im[0] = v + F;
+    if (g.d == 3) { in.re[1] = v + 2 * F; in.im[1] = nullptr; }
   }
-  RealOut out{{u, g.d == 3 ? u + 2 * g.F : nullptr, nullptr}, {u + g.F, nullptr, nullptr}};
-  TOPT_DISPATCH_N2(g.nx, (px_inv_launch<N_, double2>(g, Z, out, nf, st)));
+  const int last_axis = g.d == 3 ? 2 : 1;
+  const int Nl = g.d == 3 ? g.nz : g.ny;
+  TOPT_DISPATCH_N2(g.nx, (px_fwd_launch<N_, double2>(g, in, Z, nin, st)));
+  if (g.d == 3) TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 0, double2>(g, 1, Z, nin, nin, op, st)));
+  if (leray) TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 5, double2>(g, last_axis, Z, nin, nout, op, st)));
+  else TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 2, double2>(g, last_axis, Z, nin, nout, op, st)));
+  if (g.d == 3) TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 1, double2>(g, 1, Z, nout, nout, op, st)));
+  RealOut out{{u, g.d == 3 ? u + 2 * F : nullptr, nullptr}, {u + F, nullptr, nullptr}};
+  TOPT_DISPATCH_N2(g.nx, (px_inv_launch<N_, double2>(g, Z, out, nout, st)));
 }
 
 // b-chain up to (not including) the x^-1 pass, which the assembly kernel performs.
+// Zb: 4 float2 fields of F.
 void launch_bchain(const Geom& g, const float* b, float2* Zb, double alpha, int p, bool leray, cudaStream_t st) {
   const size_t F = g.F;
   SpecOp op{alpha, p, 1.0 / (double)F};
-  ZList<float2> Z{{Zb, Zb + F, Zb + 2 * F}};
-  int nf;
+  ZList<float2> Z{{Zb, Zb + F, Zb + 2 * F, Zb + 3 * F}};
+  int nin, nout;
   RealIn in{};
   if (leray) {
-    nf = g.d;
+    nin = g.d;
+    nout = g.d == 3 ? 4 : 2;
     for (int c = 0; c < g.d; ++c) { in.re[c] = b + c * F; in.im[c] = nullptr; }
   } else {
-    nf = g.d == 3 ? 2 : 1;
+    nin = nout = g.d == 3 ? 2 : 1;
     in.re[0] = b; in.im[0] = b + F;
     if (g.d == 3) { in.re[1] = b + 2 * F; in.im[1] = nullptr; }
   }
-  TOPT_DISPATCH_N2(g.nx, (px_fwd_launch<N_, float2>(g, in, Z, nf, st)));
+  TOPT_DISPATCH_N2(g.nx, (px_fwd_launch<N_, float2>(g, in, Z, nin, st)));
   const int last_axis = g.d == 3 ? 2 : 1;
   const int Nl = g.d == 3 ? g.nz : g.ny;
-  if (g.d == 3) TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 0, float2>(g, 1, Z, nf, op, st)));
-  if (leray) {
-    TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 4, float2>(g, last_axis, Z, nf, op, st)));
-  } else {
-    TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 3, float2>(g, last_axis, Z, nf, op, st)));
-  }
-  if (g.d == 3) TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 1, float2>(g, 1, Z, nf, op, st)));
+  if (g.d == 3) TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 0, float2>(g, 1, Z, nin, nin, op, st)));
+  if (leray) TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 4, float2>(g, last_axis, Z, nin, nout, op, st)));
+  else TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 3, float2>(g, last_axis, Z, nin, nout, op, st)));
+  if (g.d == 3) TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 1, float2>(g, 1, Z, nout, nout, op, st)));
 }
 
 template <int N>
 static void assemble_launch(const Geom& g, bool leray, const AsmArgs& a, int* nparts, cudaStream_t st) {
   using L = LineCfg<N>;
-  const int lpr = leray ? g.d : (g.d == 3 ? 2 : 1);
+  const int half = g.d == 3 ? 2 : 1;
+  const int lpr = leray ? 2 * half : half;
   int RB = L::LPB / lpr;
   if (RB < 1) RB = 1;
   const size_t sm = smem_lines<N, float2>(RB * lpr);
@@ -678,7 +703,7 @@ static void assemble_launch(const Geom& g, bool leray, const AsmArgs& a, int* np
 void launch_assemble(const Geom& g, const float2* Zb, bool leray, const float* b, const float* u, const float* v,
                      const double* vsum, float* gout, float* sout, double* partials, int* nparts, cudaStream_t st) {
   const size_t F = g.F;
-  AsmArgs a{{Zb, Zb + F, Zb + 2 * F}, b, u, v, vsum, gout, sout, partials};
+  AsmArgs a{{Zb, Zb + F, Zb + 2 * F, Zb + 3 * F}, b, u, v, vsum, gout, sout, partials};
   TOPT_DISPATCH_N2(g.nx, (assemble_launch<N_>(g, leray, a, nparts, st)));
 }
 
