@@ -652,8 +652,11 @@ void launch_vchain(const Geom& g, const float* v, double2* Zv, float* u, double 
   const int Nl = g.d == 3 ? g.nz : g.ny;
   TOPT_DISPATCH_N2(g.nx, (px_fwd_launch<N_, double2>(g, in, Z, nin, st)));
   if (g.d == 3) TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 0, double2>(g, 1, Z, nin, nin, op, st)));
-  if (leray) TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 5, double2>(g, last_axis, Z, nin, nout, op, st)));
-  else TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 2, double2>(g, last_axis, Z, nin, nout, op, st)));
+  if (leray) {
+    TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 5, double2>(g, last_axis, Z, nin, nout, op, st)));
+  } else {
+    TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 2, double2>(g, last_axis, Z, nin, nout, op, st)));
+  }
   if (g.d == 3) TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 1, double2>(g, 1, Z, nout, nout, op, st)));
   RealOut out{{u, g.d == 3 ? u + 2 * F : nullptr, nullptr}, {u + F, nullptr, nullptr}};
   TOPT_DISPATCH_N2(g.nx, (px_inv_launch<N_, double2>(g, Z, out, nout, st)));
@@ -680,8 +683,11 @@ void launch_bchain(const Geom& g, const float* b, float2* Zb, double alpha, int 
   const int last_axis = g.d == 3 ? 2 : 1;
   const int Nl = g.d == 3 ? g.nz : g.ny;
   if (g.d == 3) TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 0, float2>(g, 1, Z, nin, nin, op, st)));
-  if (leray) TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 4, float2>(g, last_axis, Z, nin, nout, op, st)));
-  else TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 3, float2>(g, last_axis, Z, nin, nout, op, st)));
+  if (leray) {
+    TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 4, float2>(g, last_axis, Z, nin, nout, op, st)));
+  } else {
+    TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 3, float2>(g, last_axis, Z, nin, nout, op, st)));
+  }
   if (g.d == 3) TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 1, float2>(g, 1, Z, nout, nout, op, st)));
 }
 
