@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""bench.py — gradient evaluations/s of the GA-NGMRES hot path on B200.
+
+Metric (BASELINE.json): "gradient evals/s at 256^3 (fwd+adj+precond), % HBM roofline,
+1/2/4/8 GPU".  Workload at N=1: BASELINE config 4 (256^3, continuity model, n_t = 8,
+H2, alpha = 1e-3) — one step = one full objective-plus-gradient evaluation through the
+C ABI (topt_eval_gradient: trace, forward SL sweep + objective, adjoint sweep, body
+force, alpha L v and the preconditioner), inputs resident in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl topt|reference]
+
+N > 1 (torchrun): every rank evaluates its own replica of the workload (weak scaling,
+no data-path collective; the z-slab path is not built yet — DESIGN.md §9); value =
+evaluations of all ranks / max-over-ranks device time.
+
+--impl reference: the fp64 CPU oracle (oracle/, test infrastructure) timed on the host
+cores on a bounded sample of the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "gradient evals/s at 256^3 (fwd+adj+precond), % HBM roofline, 1/2/4/8 GPU"
+UNIT = "evals/s"
+CONFIG = 4
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _pass_model_bytes(cfg):
+    """SURVEY §8(d) pass model, bytes per evaluation: d=3 A/C: (23 S + 53) F; I: (22 S + 38) F;
+    d=2 A: (18 S + 38) F; F = 4 n bytes."""
+    n = 1
+    for x in cfg["n"]:
+        n *= x
+    F = 4.0 * n
+    S = cfg["nt"]
+    if len(cfg["n"]) == 2:
+        return (18 * S + 38) * F
+    if cfg["model"] == 2:
+        return (22 * S + 38) * F
+    return (23 * S + 53) * F
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons, sampled every 100 ms while running."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = max(smax, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist_init():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    return rank, world, local
+
+
+def _cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_eval_rate(n_sample, device):
+    """One fp64 oracle evaluation of the config-4 recipe at n_sample^3: returns (seconds, scale)."""
+    from oracle import gradient as ogr
+    from oracle.spectral import Grid
+    from synth import make_problem
+    import numba
+    numba.set_num_threads(_cpu_threads())
+    # JIT warm-up at a tiny size (not timed)
+    dw = make_problem(CONFIG, (16, 16, 16), device=device)
+    ogr.evaluate(ogr.Problem(Grid((16, 16, 16)), dw["m0"], dw["m1"], dw["alpha"], dw["nt"], dw["model"],
+                             dw["reg_order"]), dw["vstar"])
+    d = make_problem(CONFIG, (n_sample,) * 3, device=device)
+    prob = ogr.Problem(Grid((n_sample,) * 3), d["m0"], d["m1"], d["alpha"], d["nt"], d["model"], d["reg_order"])
+    t0 = time.perf_counter()
+    ogr.evaluate(prob, d["vstar"])
+    return time.perf_counter() - t0, prob
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    import torch
+    from oracle import gradient as ogr
+    from oracle.spectral import Grid
+    from synth import make_problem
+    import numba
+    numba.set_num_threads(_cpu_threads())
+    dev = "cuda:0" if torch.cuda.is_available() else "cpu"
+    # size the per-step sample so the whole run stays within ~3 minutes
+    budget = 150.0
+    steps = args.steps + args.warmup
+    t_probe, _ = oracle_eval_rate(32, dev)
+    per_point = t_probe / 32 ** 3
+    n_s = 128
+    while n_s > 32 and steps * per_point * n_s ** 3 * 1.3 > budget:
+        n_s -= 16
+    d = make_problem(CONFIG, (n_s,) * 3, device=dev)
+    prob = ogr.Problem(Grid((n_s,) * 3), d["m0"], d["m1"], d["alpha"], d["nt"], d["model"], d["reg_order"])
+    for _ in range(args.warmup):
+        ogr.evaluate(prob, d["vstar"])
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ogr.evaluate(prob, d["vstar"])
+        ts.append(time.perf_counter() - t0)
+    scale = (n_s / 256.0) ** 3
+    sec = sum(ts) / len(ts)
+    value = scale / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config4_256^3_continuity_nt8_H2_alpha1e-3", "grid": [256, 256, 256]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": _cpu_threads(), "kind": "oracle",
+                         "sample": f"one fp64 oracle evaluation of the config-4 recipe at {n_s}^3 per step "
+                                   f"(rate scaled by ({n_s}/256)^3 to the 256^3 workload)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_topt(args):
+    import numpy as np
+    import torch
+    import paper_2510_08782_b200 as topt
+    from synth import make_problem
+
+    rank, world, local = _dist_init()
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    n = tuple(args.n) if args.n else None
+    d = make_problem(args.config, n, device=str(dev))
+    cfgp = dict(n=tuple(d["n"]), nt=d["nt"], model=d["model"], reg_order=d["reg_order"], alpha=d["alpha"])
+    t = topt.Topt(topt.Config(window=d["window"], **cfgp), device=dev)
+    m0 = torch.tensor(d["m0"], dtype=torch.float32, device=dev)
+    m1 = torch.tensor(d["m1"], dtype=torch.float32, device=dev)
+    v = torch.tensor(d["vstar"], dtype=torch.float32, device=dev)  # representative displacement
+    g = torch.empty_like(v)
+    s = torch.empty_like(v)
+    sc = torch.zeros(16, dtype=torch.float64, device=dev)
+    npts = int(np.prod(d["n"]))
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            t.eval_gradient(m0, m1, v, g, s, sc)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        l0 = topt.Topt.launch_count()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            t.eval_gradient(m0, m1, v, g, s, sc)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        launches = topt.Topt.launch_count() - l0
+        ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_per_step = ms / args.steps
+    value = world * args.steps / (ms / 1e3)
+
+    # per-kernel-class breakdown, separate (un-timed) pass with event brackets
+    t.profile(True)
+    for _ in range(args.steps):
+        t.eval_gradient(m0, m1, v, g, s, sc)
+    stats = t.kernel_stats()
+    t.profile(False)
+    peak, peak_kind = _peaks()
+    kern = [x for x in stats if x["ms"] > 0]
+    total_ms = sum(x["ms"] for x in kern)
+    dom = max((x for x in kern if x["bytes"] > 0), key=lambda x: x["ms"])
+    achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tr = json.load(open(tpath))
+            ent = tr.get("classes", {}).get(dom["name"])
+            if ent and ent.get("grid") == list(d["n"]):
+                traffic = ent.get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    per_launch_bytes = dom["bytes"] / max(1, dom["launches"])
+    roofline = {"bound": "hbm", "kernel": dom["name"], "achieved": round(achieved, 1), "peak": peak,
+                "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                "algorithmic_bytes_per_launch": per_launch_bytes, "peak_kind": peak_kind,
+                "share_of_step": round(dom["ms"] / total_ms, 4) if total_ms else None}
+    breakdown = {x["name"]: {"share": round(x["ms"] / total_ms, 4),
+                             "GB/s": round(x["bytes"] / (x["ms"] / 1e3) / 1e9, 1) if x["bytes"] else None,
+                             "launches_per_step": x["launches"] / args.steps} for x in kern}
+    model_bytes = _pass_model_bytes(cfgp)
+
+    # end to end through the public API with HOST buffers (pinned): H2D m0, m1, v; D2H g + scalars
+    e2e = None
+    if not args.no_e2e:
+        m0h = torch.tensor(d["m0"], dtype=torch.float32).pin_memory()
+        m1h = torch.tensor(d["m1"], dtype=torch.float32).pin_memory()
+        vh = torch.tensor(d["vstar"], dtype=torch.float32).pin_memory()
+        gh = torch.empty_like(vh).pin_memory()
+        sch = torch.zeros(16, dtype=torch.float64).pin_memory()
+        for _ in range(max(1, args.warmup)):
+            t.eval_gradient_host(m0h, m1h, vh, gh, sch)
+        barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            t.eval_gradient_host(m0h, m1h, vh, gh, sch)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ems = f0.elapsed_time(f1)
+        if world > 1:
+            tt = torch.tensor([ems], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            ems = float(tt.item())
+        e2e = {"value": world * args.steps / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(4 * npts * (2 + len(d["n"]))),
+               "d2h_bytes_per_step": int(4 * npts * len(d["n"]) + 16 * 8)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        sec, _ = oracle_eval_rate(args.cpu_n, str(dev))
+        scale = (args.cpu_n / d["n"][0]) ** 3
+        cpu = {"value": scale / sec, "unit": UNIT, "cores": _cpu_threads(), "kind": "oracle",
+               "sample": f"one fp64 oracle evaluation (oracle/, numba + numpy, as it stands) of the config-4 recipe "
+                         f"at {args.cpu_n}^3, rate scaled by ({args.cpu_n}/{d['n'][0]})^3 to the {d['n'][0]}^3 workload"}
+
+    if rank == 0:
+        wl = {1: "config1_2D_64^2_advection_nt4_H2", 2: "config2_64^3_advection_nt4_H1",
+              3: "config3_128^3_incompressible_nt8_H2", 4: "config4_256^3_continuity_nt8_H2_alpha1e-3",
+              5: "config5_512^3_advection_nt16_H2"}[args.config]
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": wl, "grid": list(d["n"]), "nt": d["nt"], "model": d["model"],
+                       "reg_order": d["reg_order"], "alpha": d["alpha"],
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (~15 GB of HBM traffic per evaluation vs 126 MB L2)"},
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "hbm_frac_pass_model": round(model_bytes * value / (world * peak * 1e9), 4),
+            "pass_model_bytes_per_eval": model_bytes,
+            "kernels": breakdown,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="topt", choices=["topt", "reference"])
+    ap.add_argument("--config", type=int, default=CONFIG)
+    ap.add_argument("--n", type=int, nargs="*", default=None, help="override grid (paper order)")
+    ap.add_argument("--cpu-n", type=int, default=128, help="oracle sample grid for cpu_baseline")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_topt(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -212,6 +212,23 @@ topt_status topt_multidot(topt_ctx* ctx, const float* a, const float* const* bs,
 topt_status topt_mix(topt_ctx* ctx, const float* q, const float* const* vs, const double* beta,
                      int32_t count, float* out, void* stream);
 
+/* ---- instrumentation -------------------------------------------------------------------- */
+
+/* enable != 0: bracket every launch group of the hot path with CUDA events on the caller's
+ * stream (adds event records; use a separate, un-timed pass).  Clears accumulated stats.
+ * Synchronizes the device. */
+topt_status topt_profile(topt_ctx* ctx, int32_t enable);
+
+/* Accumulated stats of kernel class `cls` (0..10; TOPT_ERR_INVALID_ARG past the end): class
+ * name (static string), total event-timed ms, total ALGORITHMIC bytes (each operand read
+ * once, each result written once per launch) and kernel launches.
+ * Synchronizes on the recorded events. */
+topt_status topt_kernel_stats(topt_ctx* ctx, int32_t cls, const char** name, double* ms, double* bytes,
+                              int64_t* launches);
+
+/* Number of kernels this library has launched since it was loaded (all contexts). */
+int64_t topt_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -193,6 +193,29 @@ class Topt:
         check(LIB.topt_mix(self.ctx, _ptr(q), arr, b, len(vs), _ptr(out), _stream()), "topt_mix")
         return out
 
+    # -- instrumentation
+    def profile(self, enable: bool = True):
+        check(LIB.topt_profile(self.ctx, 1 if enable else 0), "topt_profile")
+
+    def kernel_stats(self):
+        """Per kernel class: name, event-timed ms, algorithmic bytes, launches (since profile())."""
+        out = []
+        cls = 0
+        while True:
+            name = ctypes.c_char_p()
+            ms, by, nl = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+            st = LIB.topt_kernel_stats(self.ctx, cls, ctypes.byref(name), ctypes.byref(ms), ctypes.byref(by),
+                                       ctypes.byref(nl))
+            if st != 0:
+                break
+            out.append({"name": name.value.decode(), "ms": ms.value, "bytes": by.value, "launches": nl.value})
+            cls += 1
+        return out
+
+    @staticmethod
+    def launch_count() -> int:
+        return int(LIB.topt_launch_count())
+
     # -- solver
     def set_step_replay(self, rhos):
         arr = (ctypes.c_double * max(1, len(rhos)))(*[float(r) for r in rhos])

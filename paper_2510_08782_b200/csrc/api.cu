@@ -74,6 +74,13 @@ struct topt_ctx {
   double* dots{};  // kMaxVecs doubles
   bool have_eval = false;
   std::vector<double> replay;
+  // per-kernel-class timing (topt_profile / topt_kernel_stats)
+  bool prof = false;
+  struct Rec { int cls; cudaEvent_t a, b; double bytes; int launches; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  double pms[16]{}, pbytes[16]{};
+  long long plaunch[16]{};
 #ifdef TOPT_WITH_NCCL
   ncclComm_t comm = nullptr;
 #endif
@@ -199,6 +206,8 @@ topt_status topt_create(const topt_params* p, int32_t rank, int32_t world, const
 
 topt_status topt_destroy(topt_ctx* ctx) {
   if (!ctx) return fail(TOPT_ERR_INVALID_ARG, "ctx is NULL");
+  for (auto& r : ctx->recs) { ctx->pool.push_back(r.a); ctx->pool.push_back(r.b); }
+  for (auto e : ctx->pool) cudaEventDestroy(e);
 #ifdef TOPT_WITH_NCCL
   if (ctx->comm) ncclCommDestroy(ctx->comm);
 #endif
@@ -261,6 +270,49 @@ namespace {
 
 constexpr int kSet = 32;  // doubles per scalar set: [0, 16) public, [16, 32) internal
 
+// Kernel classes for topt_kernel_stats; bytes are ALGORITHMIC (each operand read once,
+// each result written once per launch group).
+enum KClass { K_TRACE, K_SL_FWD, K_SL_LAST, K_SL_ADJ, K_EFACTOR, K_DIV, K_BODY, K_VCHAIN, K_BCHAIN, K_ASSEMBLE,
+              K_MISC, K_NCLASS };
+const char* kClassNames[K_NCLASS] = {"sl_trace",  "sl_step_fwd", "sl_step_last", "sl_step_adj",
+                                     "efactor",   "div_v",       "body_force",   "vchain_alphaLv",
+                                     "bchain_fft", "assemble",   "misc"};
+
+cudaEvent_t take_event(topt_ctx* c) {
+  if (!c->pool.empty()) {
+    cudaEvent_t e = c->pool.back();
+    c->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// RAII scope: when profiling, brackets the enclosed launches with events on `st`
+struct Prof {
+  topt_ctx* c;
+  int cls;
+  double bytes;
+  int nl;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  Prof(topt_ctx* c_, int cls_, double bytes_, int nl_, cudaStream_t st_)
+      : c(c_), cls(cls_), bytes(bytes_), nl(nl_), st(st_) {
+    if (c->prof) {
+      a = take_event(c);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~Prof() {
+    if (c->prof) {
+      cudaEvent_t b = take_event(c);
+      cudaEventRecord(b, st);
+      c->recs.push_back({cls, a, b, bytes, nl});
+    }
+  }
+};
+
 topt_status need_ws(topt_ctx* c) {
   if (!c) return fail(TOPT_ERR_INVALID_ARG, "ctx is NULL");
   if (!c->ws) return fail(TOPT_ERR_WORKSPACE, "no workspace bound");
@@ -288,19 +340,41 @@ void forward_half(topt_ctx* c, const float* m0, const float* m1, const float* v,
   const Geom& g = c->g;
   const int S = c->p.nt;
   const size_t F = c->F;
+  const double F4 = 4.0 * F, d = c->d;
   int np = 0;
-  launch_trace(g, v, c->df, want_adj ? c->da : nullptr, c->partials, &np, st);
-  launch_finalize_slots(c->partials, 0, c->d, np, false, isc + I_SUMV, st);
+  {
+    Prof pr(c, K_TRACE, (d + d * (want_adj ? 2 : 1)) * F4, 1, st);
+    launch_trace(g, v, c->df, want_adj ? c->da : nullptr, c->partials, &np, st);
+  }
+  {
+    Prof pr(c, K_MISC, 0.0, 1, st);
+    launch_finalize_slots(c->partials, 0, c->d, np, false, isc + I_SUMV, st);
+  }
   const float* Ef = nullptr;
   if (c->p.model == TOPT_CONTINUITY) {
-    compute_div(c, v, st);
+    {
+      Prof pr(c, K_DIV, (3.0 * d - 1.0) * F4, c->d, st);
+      compute_div(c, v, st);
+    }
+    Prof pr(c, K_EFACTOR, (d + 2) * F4, 1, st);
     launch_efactor(g, c->divv, c->df, (float)(-0.5 * c->dt), (float)(0.5 * c->dt * c->dt), c->E, st);
     Ef = c->E;
   }
-  cudaMemcpyAsync(c->m_traj, m0, F * 4, cudaMemcpyDeviceToDevice, st);
-  for (int j = 0; j + 1 < S; ++j) launch_sl_step(g, c->m_traj + j * F, c->df, Ef, c->m_traj + (j + 1) * F, st);
-  launch_sl_last(g, c->m_traj + (S - 1) * F, c->df, Ef, m1, c->m_traj + S * F, c->lam_traj + S * F, c->partials,
-                 &np, st);
+  const double e = Ef ? 1.0 : 0.0;
+  {
+    Prof pr(c, K_MISC, 2.0 * F4, 0, st);
+    cudaMemcpyAsync(c->m_traj, m0, F * 4, cudaMemcpyDeviceToDevice, st);
+  }
+  for (int j = 0; j + 1 < S; ++j) {
+    Prof pr(c, K_SL_FWD, (d + 2 + e) * F4, 1, st);
+    launch_sl_step(g, c->m_traj + j * F, c->df, Ef, c->m_traj + (j + 1) * F, st);
+  }
+  {
+    Prof pr(c, K_SL_LAST, (d + 4 + e) * F4, 1, st);
+    launch_sl_last(g, c->m_traj + (S - 1) * F, c->df, Ef, m1, c->m_traj + S * F, c->lam_traj + S * F, c->partials,
+                   &np, st);
+  }
+  Prof pr(c, K_MISC, 0.0, 1, st);
   launch_finalize(c->partials, 0, np, 0.5 * c->cellvol, false, scal + TOPT_S_DIST, st);
 }
 
@@ -313,30 +387,56 @@ void backward_half(topt_ctx* c, const float* v, const float* u, float* gout, flo
   const Geom& g = c->g;
   const int S = c->p.nt;
   const size_t F = c->F;
+  const double F4 = 4.0 * F, d = c->d;
   const float* Ea = nullptr;
   if (c->p.model == TOPT_ADVECTION) {
-    compute_div(c, v, st);
+    {
+      Prof pr(c, K_DIV, (3.0 * d - 1.0) * F4, c->d, st);
+      compute_div(c, v, st);
+    }
+    Prof pr(c, K_EFACTOR, (d + 2) * F4, 1, st);
     launch_efactor(g, c->divv, c->da, (float)(0.5 * c->dt), (float)(0.5 * c->dt * c->dt), c->E, st);
     Ea = c->E;
   }
-  for (int j = S - 1; j >= 0; --j) launch_sl_step(g, c->lam_traj + (j + 1) * F, c->da, Ea, c->lam_traj + j * F, st);
+  const double e = Ea ? 1.0 : 0.0;
+  for (int j = S - 1; j >= 0; --j) {
+    Prof pr(c, K_SL_ADJ, (d + 2 + e) * F4, 1, st);
+    launch_sl_step(g, c->lam_traj + (j + 1) * F, c->da, Ea, c->lam_traj + j * F, st);
+  }
   std::vector<double> w = c->wts;
   const bool cont = c->p.model == TOPT_CONTINUITY;
   if (cont)
     for (auto& x : w) x = -x;
   for (int a = 0; a < c->d; ++a) {
+    Prof pr(c, K_BODY, (2.0 * (S + 1) + 1.0) * F4, 1, st);
     DerivArgs da{cont ? c->lam_traj : c->m_traj, F, cont ? c->m_traj : c->lam_traj, F, w.data(), S + 1, 0.f,
                  c->b + a * F};
     launch_deriv_accum(g, a, da, st);
   }
+  const bool leray = c->p.model == TOPT_INCOMPRESSIBLE;
+  const double half = c->d == 3 ? 2.0 : 1.0;
   if (!u) {
-    launch_vchain(g, v, c->Zv, c->utmp, c->p.alpha, c->p.reg_order, c->p.model == TOPT_INCOMPRESSIBLE, st);
+    const double nin = leray ? d : half, nout = half, F16 = 16.0 * F;
+    const double bytes = d * F4 + nin * F16 + (c->d == 3 ? 2 * nin * F16 + 2 * nout * F16 : 0.0) +
+                         (nin + nout) * F16 + nout * F16 + d * F4;
+    Prof pr(c, K_VCHAIN, bytes, c->d == 3 ? 5 : 3, st);
+    launch_vchain(g, v, c->Zv, c->utmp, c->p.alpha, c->p.reg_order, leray, st);
     u = c->utmp;
   }
-  const bool leray = c->p.model == TOPT_INCOMPRESSIBLE;
-  launch_bchain(g, c->b, c->Z, c->p.alpha, c->p.reg_order, leray, st);
+  {
+    const double nin = leray ? d : half, nout = leray ? 2 * half : half, F8 = 8.0 * F;
+    const double bytes = d * F4 + nin * F8 + (c->d == 3 ? 2 * nin * F8 + 2 * nout * F8 : 0.0) + (nin + nout) * F8;
+    Prof pr(c, K_BCHAIN, bytes, c->d == 3 ? 4 : 2, st);
+    launch_bchain(g, c->b, c->Z, c->p.alpha, c->p.reg_order, leray, st);
+  }
   int np = 0;
-  launch_assemble(g, c->Z, leray, c->b, u, v, isc + I_SUMV, gout, sout, c->partials, &np, st);
+  {
+    const double nout = leray ? 2 * half : half;
+    const double bytes = nout * 8.0 * F + (leray ? 0.0 : d * F4) + 2 * d * F4 + 2 * d * F4;
+    Prof pr(c, K_ASSEMBLE, bytes, 1, st);
+    launch_assemble(g, c->Z, leray, c->b, u, v, isc + I_SUMV, gout, sout, c->partials, &np, st);
+  }
+  Prof pr(c, K_MISC, 0.0, 2, st);
   launch_finalize_slots(c->partials, 0, 10, np, true, isc + I_GMAX, st);
   launch_finish(isc, scal, c->d, (double)F, c->cellvol, st);
 }
@@ -597,6 +697,40 @@ topt_status topt_mix(topt_ctx* c, const float* q, const float* const* vs, const 
   TOPT_CHECK_LAUNCH();
   return TOPT_OK;
 }
+
+topt_status topt_profile(topt_ctx* c, int32_t enable) {
+  if (!c) return fail(TOPT_ERR_INVALID_ARG, "ctx is NULL");
+  TOPT_CUDA(cudaDeviceSynchronize());
+  for (auto& r : c->recs) { c->pool.push_back(r.a); c->pool.push_back(r.b); }
+  c->recs.clear();
+  for (int i = 0; i < 16; ++i) { c->pms[i] = 0.0; c->pbytes[i] = 0.0; c->plaunch[i] = 0; }
+  c->prof = enable != 0;
+  return TOPT_OK;
+}
+
+topt_status topt_kernel_stats(topt_ctx* c, int32_t cls, const char** name, double* ms, double* bytes,
+                              int64_t* launches) {
+  if (!c) return fail(TOPT_ERR_INVALID_ARG, "ctx is NULL");
+  if (cls < 0 || cls >= K_NCLASS) return fail(TOPT_ERR_INVALID_ARG, "class out of range");
+  for (auto& r : c->recs) {
+    TOPT_CUDA(cudaEventSynchronize(r.b));
+    float t = 0.f;
+    TOPT_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    c->pms[r.cls] += t;
+    c->pbytes[r.cls] += r.bytes;
+    c->plaunch[r.cls] += r.launches;
+    c->pool.push_back(r.a);
+    c->pool.push_back(r.b);
+  }
+  c->recs.clear();
+  if (name) *name = kClassNames[cls];
+  if (ms) *ms = c->pms[cls];
+  if (bytes) *bytes = c->pbytes[cls];
+  if (launches) *launches = c->plaunch[cls];
+  return TOPT_OK;
+}
+
+int64_t topt_launch_count(void) { return (int64_t)launch_count(); }
 
 topt_status topt_set_step_replay(topt_ctx* c, const double* rho, int32_t count) {
   if (!c || count < 0 || (count && !rho)) return fail(TOPT_ERR_INVALID_ARG, "bad argument");

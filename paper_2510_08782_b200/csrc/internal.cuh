@@ -37,6 +37,8 @@ constexpr int kMaxVecs = 64;     // pointers per multidot / mix call
 struct VecList { const float* p[kMaxVecs]; float c[kMaxVecs]; };
 
 void upload_twiddles();
+void count_launch();          // one per kernel launch (all wrappers)
+long long launch_count();
 
 // ---- semi-Lagrangian kernels (kernels_sl.cu) --------------------------------------
 // Feet; when vsum_partials != null also per-block sums of v_c into slots 0..d-1 (*nparts blocks)

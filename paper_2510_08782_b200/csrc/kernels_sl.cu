@@ -209,6 +209,7 @@ void launch_trace(const Geom& g, const float* v, float* df, float* da, double* v
   if (nparts) *nparts = gr;
   if (g.d == 3) k_trace<3><<<gr, kThreads, 0, st>>>(g, v, df, da, vsum_partials);
   else k_trace<2><<<gr, kThreads, 0, st>>>(g, v, df, da, vsum_partials);
+  count_launch();
 }
 
 void launch_sl_step(const Geom& g, const float* in, const float* delta, const float* E, float* out,
@@ -221,6 +222,7 @@ void launch_sl_step(const Geom& g, const float* in, const float* delta, const fl
     if (E) k_sl_step<2, true><<<gr, kThreads, 0, st>>>(g, in, delta, E, out);
     else k_sl_step<2, false><<<gr, kThreads, 0, st>>>(g, in, delta, E, out);
   }
+  count_launch();
 }
 
 void launch_sl_last(const Geom& g, const float* in, const float* delta, const float* E,
@@ -235,12 +237,14 @@ void launch_sl_last(const Geom& g, const float* in, const float* delta, const fl
     if (E) k_sl_last<2, true><<<gr, kThreads, 0, st>>>(g, in, delta, E, m1, mS, lamS, partials);
     else k_sl_last<2, false><<<gr, kThreads, 0, st>>>(g, in, delta, E, m1, mS, lamS, partials);
   }
+  count_launch();
 }
 
 void launch_efactor(const Geom& g, const float* divv, const float* delta, float sgn_half_dt,
                     float half_dt2, float* E, cudaStream_t st) {
   if (g.d == 3) k_efactor<3><<<sl_grid(g), kThreads, 0, st>>>(g, divv, delta, sgn_half_dt, half_dt2, E);
   else k_efactor<2><<<sl_grid(g), kThreads, 0, st>>>(g, divv, delta, sgn_half_dt, half_dt2, E);
+  count_launch();
 }
 
 }  // namespace topt

@@ -259,6 +259,7 @@ static void deriv_dispatch(const Geom& g, int axis, const DerivArgs& a, const De
     k_deriv_strided<N><<<blocks, threads, sm, st>>>(g, axis, TX, a.psi, a.psi_stride, a.lam,
                                                      a.lam_stride, w, a.J, a.beta, a.out);
   }
+  count_launch();
 }
 
 #define TOPT_DISPATCH_N(NV, FN, ...)                   \
@@ -585,6 +586,7 @@ static void px_fwd_launch(const Geom& g, const RealIn& in, const ZList<C>& Z, in
   dim3 grid((unsigned)((nrows + L::LPB - 1) / L::LPB), nf);
   cudaFuncSetAttribute(k_px_fwd<N, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k_px_fwd<N, C><<<grid, kThreads, sm, st>>>(g, in, Z);
+  count_launch();
 }
 
 template <int N, typename C>
@@ -595,6 +597,7 @@ static void px_inv_launch(const Geom& g, const ZList<C>& Z, const RealOut& out, 
   dim3 grid((unsigned)((nrows + L::LPB - 1) / L::LPB), nf);
   cudaFuncSetAttribute(k_px_inv<N, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k_px_inv<N, C><<<grid, kThreads, sm, st>>>(g, Z, out);
+  count_launch();
 }
 
 template <int N, int MODE, typename C>
@@ -616,6 +619,7 @@ static void pstrided_launch(const Geom& g, int axis, const ZList<C>& Z, int nin,
   const int threads = NL * TXC * L::T;
   cudaFuncSetAttribute(k_pstrided<N, MODE, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k_pstrided<N, MODE, C><<<grid, threads, sm, st>>>(g, axis, TXC, NIN, NOUT, Z, op);
+  count_launch();
 }
 
 #define TOPT_DISPATCH_N2(NV, BODY)                                  \
@@ -704,6 +708,7 @@ static void assemble_launch(const Geom& g, bool leray, const AsmArgs& a, int* np
   *nparts = blocks;
   cudaFuncSetAttribute(k_assemble<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k_assemble<N><<<blocks, RB * lpr * L::T, sm, st>>>(g, RB, lpr, leray ? 1 : 0, a);
+  count_launch();
 }
 
 void launch_assemble(const Geom& g, const float2* Zb, bool leray, const float* b, const float* u, const float* v,

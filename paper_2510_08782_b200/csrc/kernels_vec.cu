@@ -5,9 +5,15 @@
 // in one fused pass over a and every b_i ("multi-dot"); Alg. 1 line 6 / Alg. 3
 // line 9: v^{k+1} = q + sum beta_i (q - v^{k-i}) in one pass ("mix").
 // All reductions use fp64 per-block partials and a fixed-order finalisation.
+#include <atomic>
+
 #include "internal.cuh"
 
 namespace topt {
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(); }
 
 // dst = scale * (sum or max) of partials[slot * kMaxPartials + 0 .. nparts-1]
 __global__ void k_finalize(const double* __restrict__ partials, int nparts, double scale, int is_max,
@@ -30,12 +36,14 @@ void launch_finalize(const double* partials, int slot, int nparts, double scale,
                      double* dst, cudaStream_t st) {
   k_finalize<<<1, 1024, 0, st>>>(partials + (size_t)slot * kMaxPartials, nparts, scale, is_max ? 1 : 0,
                                  dst, kMaxPartials);
+  count_launch();
 }
 
 void launch_finalize_multi(const double* partials, int slot0, int nslots, int nparts, double scale,
                            double* dst, cudaStream_t st) {
   k_finalize<<<nslots, 1024, 0, st>>>(partials + (size_t)slot0 * nparts, nparts, scale, 0, dst,
                                       (size_t)nparts);
+  count_launch();
 }
 
 __global__ void k_combine_obj(double* s) { s[TOPT_S_OBJ] = s[TOPT_S_DIST] + s[TOPT_S_REG]; }
@@ -60,6 +68,7 @@ __global__ void k_finalize_slots(const double* __restrict__ partials, int nparts
 void launch_finalize_slots(const double* partials, int first, int count, int nparts, bool first_is_max,
                            double* dst, cudaStream_t st) {
   k_finalize_slots<<<count, 1024, 0, st>>>(partials + (size_t)first * kMaxPartials, nparts, first_is_max ? 1 : 0, dst);
+  count_launch();
 }
 
 // Public scalars from the internal sums (h^d = cellvol, n = points):
@@ -78,8 +87,10 @@ __global__ void k_finish(const double* __restrict__ isc, double* __restrict__ sc
 }
 void launch_finish(const double* isc, double* sc, int d, double n, double cellvol, cudaStream_t st) {
   k_finish<<<1, 1, 0, st>>>(isc, sc, d, n, cellvol);
+  count_launch();
 }
-void launch_combine_obj(double* scalars, cudaStream_t st) { k_combine_obj<<<1, 1, 0, st>>>(scalars); }
+void launch_combine_obj(double* scalars, cudaStream_t st) { k_combine_obj<<<1, 1, 0, st>>>(scalars);   count_launch();
+}
 
 // Note: products are formed in fp32 (exact for fp32 x fp32 -> fp64 only if promoted first);
 // promote before multiplying so every product is exact in fp64.
@@ -130,7 +141,10 @@ void launch_multidot(const float* a, const float* const* bs, int count, size_t n
   *nparts = nb;
   constexpr int CH = 8;
   for (int i0 = 0; i0 < count; i0 += CH)
+  {
     k_multidot_exact<CH><<<nb, kThreads, 0, st>>>(a, L, i0, count, n4, partials);
+    count_launch();
+  }
 }
 
 // out = q + sum_i beta_i (q - v_i): the differences are formed first (no 1 + sum beta cancellation)
@@ -160,6 +174,7 @@ void launch_mix(const float* q, const float* const* vs, const double* beta, int 
   }
   const size_t n4 = n / 4;
   k_mix<<<grid_for(n4, kThreads, 148 * 8), kThreads, 0, st>>>(q, L, count, n4, out);
+  count_launch();
 }
 
 // out = x + a*y + cst_c (cst per component c = i / (n/ncomp); used for u_q = u - rho (g - gbar))
@@ -180,6 +195,7 @@ void launch_axpy_c(const float* x, float a, const float* y, size_t n, int ncomp,
   k_axpy_c<<<grid_for(n / 4, kThreads, 148 * 8), kThreads, 0, st>>>(x, a, y, n / 4, n / 4 / ncomp, cst[0],
                                                                      ncomp > 1 ? cst[1] : 0.f,
                                                                      ncomp > 2 ? cst[2] : 0.f, out);
+  count_launch();
 }
 
 __global__ void k_axpy(const float* __restrict__ x, float a, const float* __restrict__ y, size_t n4,
@@ -194,6 +210,7 @@ __global__ void k_axpy(const float* __restrict__ x, float a, const float* __rest
 }
 void launch_axpy(const float* x, float a, const float* y, size_t n, float* out, cudaStream_t st) {
   k_axpy<<<grid_for(n / 4, kThreads, 148 * 8), kThreads, 0, st>>>(x, a, y, n / 4, out);
+  count_launch();
 }
 
 __global__ void k_sub(const float* __restrict__ a, const float* __restrict__ b, size_t n4, float* __restrict__ out) {
@@ -207,6 +224,7 @@ __global__ void k_sub(const float* __restrict__ a, const float* __restrict__ b, 
 }
 void launch_sub(const float* a, const float* b, size_t n, float* out, cudaStream_t st) {
   k_sub<<<grid_for(n / 4, kThreads, 148 * 8), kThreads, 0, st>>>(a, b, n / 4, out);
+  count_launch();
 }
 
 }  // namespace topt

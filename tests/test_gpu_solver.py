@@ -12,11 +12,11 @@ from oracle import solver as osolver
 pytestmark = pytest.mark.gpu
 
 CASES = [
-    # (config recipe, grid, model override, w, sigma, tau)
+    # (config recipe, grid, alpha override, w, sigma, tau)
     (1, (64, 64), None, 5, 1, 2),          # config 1: 2D, mixing period 3
     (2, (32, 32, 32), None, 5, 1, 0),      # config 2 recipe: H1, NGMRES(5)
     (3, (32, 32, 32), None, 5, 1, 1),      # config 3 recipe: incompressible, period 2
-    (4, (32, 32, 32), None, 3, 1, 0),      # config 4 recipe: continuity, w = 3
+    (4, (32, 32, 32), 1e-4, 3, 1, 0),      # config 4 recipe: continuity, alpha 1e-4 (swept), w = 3
 ]
 
 
@@ -34,9 +34,9 @@ def _gpu_solve(d, w, sigma, tau, n_iter, eps, method=0, ordering=0, replay=None)
     return host(v), rep
 
 
-@pytest.mark.parametrize("cfg,n,model,w,sigma,tau", CASES)
-def test_twenty_iterations_match_oracle(cfg, n, model, w, sigma, tau):
-    d = case(cfg, n, model=model)
+@pytest.mark.parametrize("cfg,n,alpha,w,sigma,tau", CASES)
+def test_twenty_iterations_match_oracle(cfg, n, alpha, w, sigma, tau):
+    d = case(cfg, n, alpha=alpha)
     ref = _oracle_solve(d, w, sigma, tau, 20, 0.0)
     v, rep = _gpu_solve(d, w, sigma, tau, 20, 0.0)
     assert rep["iters"] == ref.iters == 20
@@ -47,9 +47,9 @@ def test_twenty_iterations_match_oracle(cfg, n, model, w, sigma, tau):
     assert rel_l2(v2, ref.v) <= 1e-3
 
 
-@pytest.mark.parametrize("cfg,n,model,w,sigma,tau", CASES)
-def test_iteration_count_to_tolerance(cfg, n, model, w, sigma, tau):
-    d = case(cfg, n, model=model)
+@pytest.mark.parametrize("cfg,n,alpha,w,sigma,tau", CASES)
+def test_iteration_count_to_tolerance(cfg, n, alpha, w, sigma, tau):
+    d = case(cfg, n, alpha=alpha)
     ref = _oracle_solve(d, w, sigma, tau, 60, 5e-2)
     _, rep = _gpu_solve(d, w, sigma, tau, 60, 5e-2)
     assert ref.exit == osolver.CONVERGED
