@@ -16,7 +16,10 @@ CASES = [
     (1, (64, 64), None, 5, 1, 2),          # config 1: 2D, mixing period 3
     (2, (32, 32, 32), None, 5, 1, 0),      # config 2 recipe: H1, NGMRES(5)
     (3, (32, 32, 32), None, 5, 1, 1),      # config 3 recipe: incompressible, period 2
-    (4, (32, 32, 32), 1e-4, 3, 1, 0),      # config 4 recipe: continuity, alpha 1e-4 (swept), w = 3
+    # config 4 recipe (continuity), w = 3.  alpha = 1e-5 at 32^3 keeps all 20 iterations in the descent
+    # regime; at 1e-4 the 32^3 problem reaches its fp64 noise floor after ~10 iterations (rel. grad
+    # stalls at 7e-4, obj constant to 1e-8) where v is not determined by obj.
+    (4, (32, 32, 32), 1e-5, 3, 1, 0),
 ]
 
 
