@@ -55,6 +55,15 @@ void launch_sl_last(const Geom& g, const float* in, const float* delta, const fl
 void launch_efactor(const Geom& g, const float* divv, const float* delta, float sgn_half_dt,
                     float half_dt2, float* E, cudaStream_t st);
 
+// shared-memory z-marching variants (kernels_sl_tiled.cu), used when tiled_ok(g)
+bool tiled_ok(const Geom& g);
+void tiled_trace(const Geom& g, const float* v, float* df, float* da, double* vsum, int* nparts, cudaStream_t st);
+void tiled_step(const Geom& g, const float* in, const float* delta, const float* E, float* out, cudaStream_t st);
+void tiled_last(const Geom& g, const float* in, const float* delta, const float* E, const float* m1, float* mS,
+                float* lamS, double* partials, int* nparts, cudaStream_t st);
+void tiled_efactor(const Geom& g, const float* divv, const float* delta, float sh, float h2, float* E,
+                   cudaStream_t st);
+
 // ---- spectral kernels (kernels_spectral.cu) ------------------------------------------
 // out = beta*out + sum_{j<J} w_j * (lam_j ? lam_j : 1) * d/dx_axis psi_j
 // psi_j = psi + j*psi_stride, lam_j = lam + j*lam_stride (lam may be null).

@@ -205,6 +205,10 @@ static int sl_grid(const Geom& g) { return grid_for(g.F, kThreads, 148 * 16); }
 
 void launch_trace(const Geom& g, const float* v, float* df, float* da, double* vsum_partials, int* nparts,
                   cudaStream_t st) {
+  if (tiled_ok(g)) {
+    tiled_trace(g, v, df, da, vsum_partials, nparts, st);
+    return;
+  }
   const int gr = sl_grid(g);
   if (nparts) *nparts = gr;
   if (g.d == 3) k_trace<3><<<gr, kThreads, 0, st>>>(g, v, df, da, vsum_partials);
@@ -214,6 +218,10 @@ void launch_trace(const Geom& g, const float* v, float* df, float* da, double* v
 
 void launch_sl_step(const Geom& g, const float* in, const float* delta, const float* E, float* out,
                     cudaStream_t st) {
+  if (tiled_ok(g)) {
+    tiled_step(g, in, delta, E, out, st);
+    return;
+  }
   const int gr = sl_grid(g);
   if (g.d == 3) {
     if (E) k_sl_step<3, true><<<gr, kThreads, 0, st>>>(g, in, delta, E, out);
@@ -228,6 +236,10 @@ void launch_sl_step(const Geom& g, const float* in, const float* delta, const fl
 void launch_sl_last(const Geom& g, const float* in, const float* delta, const float* E,
                     const float* m1, float* mS, float* lamS, double* partials, int* nparts,
                     cudaStream_t st) {
+  if (tiled_ok(g)) {
+    tiled_last(g, in, delta, E, m1, mS, lamS, partials, nparts, st);
+    return;
+  }
   const int gr = grid_for(g.F, kThreads, kMaxPartials);
   *nparts = gr;
   if (g.d == 3) {
@@ -242,6 +254,10 @@ void launch_sl_last(const Geom& g, const float* in, const float* delta, const fl
 
 void launch_efactor(const Geom& g, const float* divv, const float* delta, float sgn_half_dt,
                     float half_dt2, float* E, cudaStream_t st) {
+  if (tiled_ok(g)) {
+    tiled_efactor(g, divv, delta, sgn_half_dt, half_dt2, E, st);
+    return;
+  }
   if (g.d == 3) k_efactor<3><<<sl_grid(g), kThreads, 0, st>>>(g, divv, delta, sgn_half_dt, half_dt2, E);
   else k_efactor<2><<<sl_grid(g), kThreads, 0, st>>>(g, divv, delta, sgn_half_dt, half_dt2, E);
   count_launch();

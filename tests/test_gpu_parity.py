@@ -126,3 +126,15 @@ def test_underresolved_grid_conditioning():
     tol = 1e-5 + 4 * 6e-8 * d["nt"] * kappa
     assert rel_l2(host(lam)[-1], ref["lam"][-1]) < tol
     assert rel_l2(host(b), ref["b"]) < 4 * tol
+
+
+def test_forward_large_displacement_fallback():
+    """Feet beyond the shared-memory halo (|delta| > 3 cells) take the L1 fallback path inside
+    the tiled kernel; SL is unconditionally stable, so any CFL must be exact."""
+    d = case(2, (32, 32, 32), scale=4.0)
+    rf, _ = transport.feet(d["grid"], d["v"], d["nt"])
+    assert np.max(np.abs(rf)) > 4.0
+    t = topt_for(d)
+    traj = host(t.forward(dev(d["m0"]), dev(d["v"])))
+    _, _, _, ref = ogr.forward_solve(d["prob"], d["v"])
+    assert rel_l2(traj[-1], ref[-1]) < TOL
