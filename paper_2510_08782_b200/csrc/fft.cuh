@@ -19,7 +19,7 @@
 
 namespace topt {
 
-__host__ __device__ constexpr int fft_threads(int n) { return n >= 16 ? n / 16 : 1; }
+__host__ __device__ constexpr int fft_threads(int n, int rmax = 16) { return n >= rmax ? n / rmax : 1; }
 __host__ __device__ constexpr int fft_pad(int i) { return i + (i >> 4); }
 __host__ __device__ constexpr int fft_line_stride(int n) { return n + n / 16 + 1; }
 
@@ -137,10 +137,10 @@ struct Dft<16, INV, C> {
 // One Stockham stage on a padded line `buf`, done by T threads (tid < T).
 // tw: table of exp(-2 pi i m / N), m = 0..N-1.
 // All threads of the block must call it (it contains __syncthreads); `active` masks work.
-template <int N, int R, int NS, bool INV, typename C>
+template <int N, int R, int NS, bool INV, typename C, int RMAX>
 __device__ __forceinline__ void fft_stage(C* buf, const C* tw, int tid, bool active) {
   constexpr int M = N / R;
-  constexpr int T = fft_threads(N);
+  constexpr int T = fft_threads(N, RMAX);
   constexpr int NB = M / T;  // butterflies per thread
   C a[NB][R];
   if (active) {
@@ -174,24 +174,25 @@ __device__ __forceinline__ void fft_stage(C* buf, const C* tw, int tid, bool act
   __syncthreads();
 }
 
-template <int N, int NS, bool INV, typename C>
+template <int N, int NS, bool INV, typename C, int RMAX>
 struct FftStages {
   static __device__ __forceinline__ void run(C* buf, const C* tw, int tid, bool active) {
     constexpr int REM = N / NS;
-    constexpr int R = REM >= 16 ? 16 : REM;
-    fft_stage<N, R, NS, INV, C>(buf, tw, tid, active);
-    FftStages<N, NS * R, INV, C>::run(buf, tw, tid, active);
+    constexpr int R = REM >= RMAX ? RMAX : REM;
+    fft_stage<N, R, NS, INV, C, RMAX>(buf, tw, tid, active);
+    FftStages<N, NS * R, INV, C, RMAX>::run(buf, tw, tid, active);
   }
 };
-template <int N, bool INV, typename C>
-struct FftStages<N, N, INV, C> {
+template <int N, bool INV, typename C, int RMAX>
+struct FftStages<N, N, INV, C, RMAX> {
   static __device__ __forceinline__ void run(C*, const C*, int, bool) {}
 };
 
-// Unnormalised DFT (forward: exp(-i k x), inverse: exp(+i k x)) of a padded smem line.
-template <int N, bool INV, typename C>
+// Unnormalised DFT (forward: exp(-i k x), inverse: exp(+i k x)) of a padded smem line by
+// fft_threads(N, RMAX) threads (max radix RMAX in {8, 16}).
+template <int N, bool INV, int RMAX = 16, typename C>
 __device__ __forceinline__ void fft_line(C* buf, const C* tw, int tid, bool active) {
-  FftStages<N, 1, INV, C>::run(buf, tw, tid, active);
+  FftStages<N, 1, INV, C, RMAX>::run(buf, tw, tid, active);
 }
 
 // Device twiddle tables: tw[N + m] = exp(-2 pi i m / N), N = 4..1024, computed in fp64

@@ -11,18 +11,25 @@
 //     delta / E / output streams stay fully coalesced;
 //   * feet whose floor offsets leave [-3, 2] in any axis (|delta| > ~3 cells) fall back to
 //     the L1 gather of kernels_sl.cu for that point (correct for any CFL).
-// Global traffic per output point ~ (1 + 0.8 per-plane halo) input floats + the streams.
+// Smem rows are padded to a 64-word pitch (bank-conflict-free when a warp straddles rows or
+// planes).  Global traffic per output point ~ 1.6 input floats (halo) + the streams.
 #include "internal.cuh"
 
 namespace topt {
 
 namespace tiled {
-constexpr int TX = 32, TY = 8, HALO = 4;
-constexpr int PW = TX + 2 * HALO;     // 40 floats per smem row
-constexpr int PH = TY + 2 * HALO;     // 16 rows per plane
-constexpr int PS = PW * PH;           // 640 floats per plane
-constexpr int NZR = 2 * HALO + 2;     // 10 ring slots
-constexpr int NLOAD = (PW / 4) * PH;  // 160 float4 per plane
+constexpr int TX = 32, TY = 8;
+constexpr int XH = 4;                 // x halo (float4 aligned): foot floors in [-3, 2]
+constexpr int XW = TX + 2 * XH;       // 40 floats loaded per row
+constexpr int PW = 64;                // smem row pitch: a multiple of 32 words, so lanes of a warp that
+                                      // straddle two rows / planes hit disjoint banks
+template <int H>                      // y/z halo: foot floors in [-H+1, H-2]
+struct Cfg {
+  static constexpr int PH = TY + 2 * H;       // rows per plane
+  static constexpr int PS = PW * PH;          // floats per plane (multiple of 32)
+  static constexpr int NZR = 2 * H + 2;       // ring slots (planes z-H .. z+H + one prefetch)
+  static constexpr int NLOAD = (XW / 4) * PH; // float4 loads per plane
+};
 }  // namespace tiled
 
 enum { M_STEP = 0, M_LAST = 1, M_EFACTOR = 2, M_TRACE = 3 };
@@ -70,9 +77,10 @@ __device__ __forceinline__ float gather_global(const Geom& g, const float* __res
   return acc;
 }
 
-template <int MODE, int NF, bool HAS_E>
+template <int MODE, int NF, bool HAS_E, int HALO>
 __global__ void __launch_bounds__(256) k_sl_tiled(Geom g, int ZC, TileArgs a) {
   using namespace tiled;
+  constexpr int PS = Cfg<HALO>::PS, NZR = Cfg<HALO>::NZR, NLOAD = Cfg<HALO>::NLOAD;
   extern __shared__ __align__(16) float sm[];  // [NF][NZR][PS]
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int tilesx = g.nx / TX, tilesy = g.ny / TY;
@@ -88,8 +96,8 @@ __global__ void __launch_bounds__(256) k_sl_tiled(Geom g, int ZC, TileArgs a) {
 
   // loader role: thread t < NLOAD owns float4 (row ld_r, chunk ld_k) of every plane
   const bool loader = threadIdx.x < NLOAD;
-  const int ld_r = threadIdx.x / (PW / 4), ld_k = threadIdx.x % (PW / 4);
-  const size_t ld_off = (size_t)((y0 - HALO + ld_r) & (g.ny - 1)) * g.nx + ((x0 - HALO + 4 * ld_k) & (g.nx - 1));
+  const int ld_r = threadIdx.x / (XW / 4), ld_k = threadIdx.x % (XW / 4);
+  const size_t ld_off = (size_t)((y0 - HALO + ld_r) & (g.ny - 1)) * g.nx + ((x0 - XH + 4 * ld_k) & (g.nx - 1));
   const int ld_s = ld_r * PW + 4 * ld_k;
 
 #pragma unroll 1
@@ -122,7 +130,7 @@ __global__ void __launch_bounds__(256) k_sl_tiled(Geom g, int ZC, TileArgs a) {
     auto gather = [&](float dx, float dy, float dz, float* res) {
       const float fx = floorf(dx), fy = floorf(dy), fz = floorf(dz);
       const int ix = (int)fx, iy = (int)fy, iz = (int)fz;
-      if (ix < -HALO + 1 || ix > HALO - 2 || iy < -HALO + 1 || iy > HALO - 2 || iz < -HALO + 1 || iz > HALO - 2) {
+      if (ix < -XH + 1 || ix > XH - 2 || iy < -HALO + 1 || iy > HALO - 2 || iz < -HALO + 1 || iz > HALO - 2) {
 #pragma unroll
         for (int f = 0; f < NF; ++f) res[f] = gather_global(g, a.in[f], x, y, z, dx, dy, dz);
         return;
@@ -131,7 +139,7 @@ __global__ void __launch_bounds__(256) k_sl_tiled(Geom g, int ZC, TileArgs a) {
       lag4(dx - fx, wx);
       lag4(dy - fy, wy);
       lag4(dz - fz, wz);
-      const int rowoff = (ty + iy - 1 + HALO) * PW + tx + ix - 1 + HALO;
+      const int rowoff = (ty + iy - 1 + HALO) * PW + tx + ix - 1 + XH;
       int s = slot0 + HALO + iz - 1;
       if (s >= NZR) s -= NZR;
 #pragma unroll
@@ -159,9 +167,10 @@ __global__ void __launch_bounds__(256) k_sl_tiled(Geom g, int ZC, TileArgs a) {
     };
 
     if (MODE == M_TRACE) {
-      const float u0 = sm[(0 * NZR + (slot0 + HALO) % NZR) * PS + (ty + HALO) * PW + tx + HALO];
-      const float u1 = sm[(1 * NZR + (slot0 + HALO) % NZR) * PS + (ty + HALO) * PW + tx + HALO];
-      const float u2 = sm[(2 * NZR + (slot0 + HALO) % NZR) * PS + (ty + HALO) * PW + tx + HALO];
+      const int cidx = ((slot0 + HALO) % NZR) * PS + (ty + HALO) * PW + tx + XH;
+      const float u0 = sm[0 * NZR * PS + cidx];
+      const float u1 = sm[1 * NZR * PS + cidx];
+      const float u2 = sm[2 * NZR * PS + cidx];
       vs0 += u0; vs1 += u1; vs2 += u2;
       const float c0 = u0 * g.cx, c1 = u1 * g.cy, c2 = u2 * g.cz;
 #pragma unroll
@@ -180,7 +189,7 @@ __global__ void __launch_bounds__(256) k_sl_tiled(Geom g, int ZC, TileArgs a) {
       float r[NF];
       gather(dx, dy, dz, r);
       if (MODE == M_EFACTOR) {
-        const float bv = sm[((slot0 + HALO) % NZR) * PS + (ty + HALO) * PW + tx + HALO];  // divv(l)
+        const float bv = sm[((slot0 + HALO) % NZR) * PS + (ty + HALO) * PW + tx + XH];  // divv(l)
         a.out[0][gi] = 1.0f + a.sh * (r[0] + bv) + a.h2 * r[0] * bv;
       } else {
         float val = r[0];
@@ -243,11 +252,12 @@ static int tiled_zc(const Geom& g) { return g.nz < 32 ? g.nz : 32; }
 
 int tiled_blocks(const Geom& g) { return (g.nx / tiled::TX) * (g.ny / tiled::TY) * (g.nz / tiled_zc(g)); }
 
-template <int MODE, int NF, bool HAS_E>
+template <int MODE, int NF, bool HAS_E, int HALO = 4>
 static void launch_tiled(const Geom& g, const TileArgs& a, cudaStream_t st) {
-  const size_t sm = (size_t)NF * tiled::NZR * tiled::PS * sizeof(float);
-  cudaFuncSetAttribute(k_sl_tiled<MODE, NF, HAS_E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_sl_tiled<MODE, NF, HAS_E><<<tiled_blocks(g), 256, sm, st>>>(g, tiled_zc(g), a);
+  using C = tiled::Cfg<HALO>;
+  const size_t sm = (size_t)NF * C::NZR * C::PS * sizeof(float);
+  cudaFuncSetAttribute(k_sl_tiled<MODE, NF, HAS_E, HALO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_sl_tiled<MODE, NF, HAS_E, HALO><<<tiled_blocks(g), 256, sm, st>>>(g, tiled_zc(g), a);
   count_launch();
 }
 
@@ -258,7 +268,7 @@ void tiled_trace(const Geom& g, const float* v, float* df, float* da, double* vs
   for (int c = 0; c < 3; ++c) a.in[c] = v + c * g.F;
   a.out[0] = df;
   a.out[1] = da;
-  launch_tiled<M_TRACE, 3, false>(g, a, st);
+  launch_tiled<M_TRACE, 3, false, 2>(g, a, st);  // midpoint displacement dt/2 v: |floor| <= 1
 }
 
 void tiled_step(const Geom& g, const float* in, const float* delta, const float* E, float* out, cudaStream_t st) {

@@ -39,9 +39,9 @@ void upload_twiddles() {
   cudaMemcpyToSymbol(g_twiddle_d, hd, sizeof(hd));
 }
 
-template <int N>
+template <int N, int RMAX = 16>
 struct LineCfg {
-  static constexpr int T = fft_threads(N);
+  static constexpr int T = fft_threads(N, RMAX);
   static constexpr int LPB = kThreads / T;           // complex lines per 256-thread block
   static constexpr int STRIDE = fft_line_stride(N);  // complex elements per smem line
 };
@@ -63,11 +63,11 @@ __device__ __forceinline__ float kprime(int q, int N) {  // Nyquist zeroed (R3)
 // IFFT(i k' FFT(a + i b)) = d a + i d b.
 // =====================================================================================
 template <int N>
-__global__ void __launch_bounds__(kThreads) k_deriv_x(Geom g, const float* __restrict__ psi,
+__global__ void __launch_bounds__(kThreads, 3) k_deriv_x(Geom g, const float* __restrict__ psi,
                                                       size_t psi_stride, const float* __restrict__ lam,
                                                       size_t lam_stride, DerivWeights w, int J,
                                                       float beta, float* __restrict__ out) {
-  using C = LineCfg<N>;
+  using C = LineCfg<N, 8>;
   extern __shared__ float2 smem[];
   float2* buf = smem;
   float2* tw = smem + C::LPB * C::STRIDE;
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(kThreads) k_deriv_x(Geom g, const float* __res
     }
     __syncthreads();
     float2* line = buf + myline * C::STRIDE;
-    fft_line<N, false>(line, tw, tid, active);
+    fft_line<N, false, 8>(line, tw, tid, active);
     if (active) {
       for (int q = tid; q < N; q += C::T) {
         const float k = kprime(q, N) * invN;
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kThreads) k_deriv_x(Geom g, const float* __res
       }
     }
     __syncthreads();
-    fft_line<N, true>(line, tw, tid, active);
+    fft_line<N, true, 8>(line, tw, tid, active);
     const float wj = w.w[j];
     const float* lj = lam ? lam + j * lam_stride : nullptr;
 #pragma unroll
@@ -147,70 +147,68 @@ __global__ void __launch_bounds__(kThreads) k_deriv_x(Geom g, const float* __res
 // tile of TX consecutive x columns x N positions; columns (2c, 2c+1) share a complex line.
 // =====================================================================================
 template <int N>
-__global__ void __launch_bounds__(kThreads) k_deriv_strided(Geom g, int axis, int TX,
-                                                            const float* __restrict__ psi,
-                                                            size_t psi_stride,
-                                                            const float* __restrict__ lam,
-                                                            size_t lam_stride, DerivWeights w, int J,
-                                                            float beta, float* __restrict__ out) {
-  using C = LineCfg<N>;
+__global__ void __launch_bounds__(kThreads, 3) k_deriv_strided(Geom g, int axis, int TX,
+                                                               const float* __restrict__ psi,
+                                                               size_t psi_stride,
+                                                               const float* __restrict__ lam,
+                                                               size_t lam_stride, DerivWeights w, int J,
+                                                               float beta, float* __restrict__ out) {
+  using C = LineCfg<N, 8>;
   extern __shared__ float2 smem[];
   float2* buf = smem;
   float2* tw = smem + C::LPB * C::STRIDE;
   load_twiddles<N>(tw);
-  const int nlines = TX / 2;
+  // all threads active: threads = (TX/2) * T, float4 per thread = N / (2T) = E4
+  constexpr int E4 = N / (2 * C::T);
+  const int TX4 = TX >> 2;
+  const int lt4 = __ffs(TX4) - 1;
   const int tilesx = g.nx / TX;
   const int x0 = (blockIdx.x % tilesx) * TX;
   const int outer = blockIdx.x / tilesx;
-  size_t base, S;
-  if (axis == 1) { base = ((size_t)outer << (g.lx + g.ly)) + x0; S = g.nx; }
-  else { base = ((size_t)outer << g.lx) + x0; S = (size_t)g.nx * g.ny; }
-  const int TX4 = TX / 4;
-  const int n4 = N * TX4;  // float4 in the tile
-  const int myline = threadIdx.x / C::T, tid = threadIdx.x % C::T;
-  const bool active = myline < nlines;
-  constexpr int MAXE = 8;  // N*TX/4 / (TX/2 * T) = N/(2T) <= 8
-  float4 acc[MAXE];
+  unsigned base, S;
+  if (axis == 1) { base = ((unsigned)outer << (g.lx + g.ly)) + x0; S = g.nx; }
+  else { base = ((unsigned)outer << g.lx) + x0; S = (unsigned)g.nx * g.ny; }
+  unsigned goff[E4];
+  int soff[E4];
 #pragma unroll
-  for (int e = 0; e < MAXE; ++e) acc[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int e = 0; e < E4; ++e) {
+    const int f4 = threadIdx.x + e * blockDim.x;
+    const int row = f4 >> lt4, c4 = f4 & (TX4 - 1);
+    goff[e] = base + row * S + 4 * c4;
+    soff[e] = (2 * c4) * C::STRIDE + fft_pad(row);
+  }
+  const int myline = threadIdx.x / C::T, tid = threadIdx.x % C::T;
+  float4 acc[E4];
+#pragma unroll
+  for (int e = 0; e < E4; ++e) acc[e] = make_float4(0.f, 0.f, 0.f, 0.f);
   const float invN = 1.0f / (float)N;
-  const int nthreads = blockDim.x;
   for (int j = 0; j < J; ++j) {
     const float* src = psi + j * psi_stride;
     __syncthreads();
 #pragma unroll
-    for (int e = 0; e < MAXE; ++e) {
-      const int f4 = threadIdx.x + e * nthreads;
-      if (f4 >= n4) break;
-      const int row = f4 / TX4, c4 = f4 % TX4;
-      const float4 val = *reinterpret_cast<const float4*>(src + base + row * S + c4 * 4);
-      float* l0 = reinterpret_cast<float*>(buf + (2 * c4) * C::STRIDE + fft_pad(row));
-      float* l1 = reinterpret_cast<float*>(buf + (2 * c4 + 1) * C::STRIDE + fft_pad(row));
-      l0[0] = val.x; l0[1] = val.y; l1[0] = val.z; l1[1] = val.w;
+    for (int e = 0; e < E4; ++e) {
+      const float4 val = __ldg(reinterpret_cast<const float4*>(src + goff[e]));
+      buf[soff[e]] = make_float2(val.x, val.y);
+      buf[soff[e] + C::STRIDE] = make_float2(val.z, val.w);
     }
     __syncthreads();
     float2* line = buf + myline * C::STRIDE;
-    fft_line<N, false>(line, tw, tid, active);
-    if (active) {
-      for (int q = tid; q < N; q += C::T) {
-        const float k = kprime(q, N) * invN;
-        const float2 z = line[fft_pad(q)];
-        line[fft_pad(q)] = make_float2(-k * z.y, k * z.x);
-      }
+    fft_line<N, false, 8>(line, tw, tid, true);
+    for (int q = tid; q < N; q += C::T) {
+      const float k = kprime(q, N) * invN;
+      const float2 z = line[fft_pad(q)];
+      line[fft_pad(q)] = make_float2(-k * z.y, k * z.x);
     }
     __syncthreads();
-    fft_line<N, true>(line, tw, tid, active);
+    fft_line<N, true, 8>(line, tw, tid, true);
     const float wj = w.w[j];
     const float* lj = lam ? lam + j * lam_stride : nullptr;
 #pragma unroll
-    for (int e = 0; e < MAXE; ++e) {
-      const int f4 = threadIdx.x + e * nthreads;
-      if (f4 >= n4) break;
-      const int row = f4 / TX4, c4 = f4 % TX4;
-      const float2 d0 = buf[(2 * c4) * C::STRIDE + fft_pad(row)];
-      const float2 d1 = buf[(2 * c4 + 1) * C::STRIDE + fft_pad(row)];
+    for (int e = 0; e < E4; ++e) {
+      const float2 d0 = buf[soff[e]];
+      const float2 d1 = buf[soff[e] + C::STRIDE];
       float4 l4 = make_float4(1.f, 1.f, 1.f, 1.f);
-      if (lj) l4 = *reinterpret_cast<const float4*>(lj + base + row * S + c4 * 4);
+      if (lj) l4 = __ldg(reinterpret_cast<const float4*>(lj + goff[e]));
       acc[e].x = fmaf(wj * l4.x, d0.x, acc[e].x);
       acc[e].y = fmaf(wj * l4.y, d0.y, acc[e].y);
       acc[e].z = fmaf(wj * l4.z, d1.x, acc[e].z);
@@ -218,11 +216,8 @@ __global__ void __launch_bounds__(kThreads) k_deriv_strided(Geom g, int axis, in
     }
   }
 #pragma unroll
-  for (int e = 0; e < MAXE; ++e) {
-    const int f4 = threadIdx.x + e * nthreads;
-    if (f4 >= n4) break;
-    const int row = f4 / TX4, c4 = f4 % TX4;
-    float4* o = reinterpret_cast<float4*>(out + base + row * S + c4 * 4);
+  for (int e = 0; e < E4; ++e) {
+    float4* o = reinterpret_cast<float4*>(out + goff[e]);
     float4 r = acc[e];
     if (beta != 0.0f) {
       const float4 p = *o;
@@ -232,17 +227,17 @@ __global__ void __launch_bounds__(kThreads) k_deriv_strided(Geom g, int axis, in
   }
 }
 
-template <int N>
+template <int N, int RMAX = 16>
 static size_t line_smem() {
-  using C = LineCfg<N>;
+  using C = LineCfg<N, RMAX>;
   return (size_t)(C::LPB * C::STRIDE + N) * sizeof(float2);
 }
 
 template <int N>
 static void deriv_dispatch(const Geom& g, int axis, const DerivArgs& a, const DerivWeights& w,
                            cudaStream_t st) {
-  using C = LineCfg<N>;
-  const size_t sm = line_smem<N>();
+  using C = LineCfg<N, 8>;
+  const size_t sm = line_smem<N, 8>();
   if (axis == 0) {
     const size_t nlines = (size_t)g.ny * g.nz;
     const int blocks = (int)((nlines + 2 * C::LPB - 1) / (2 * C::LPB));

@@ -1,0 +1,43 @@
+"""Summarise an ncu report (raw page) for the kernels in it: time, DRAM bytes, occupancy,
+pipe utilisation and the top stall reasons.  Usage: python tools/ncu_summary.py rep.ncu-rep"""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "launch__registers_per_thread",
+    "launch__grid_size", "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem", "smsp__inst_executed.sum",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "l1tex__throughput.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+]
+
+
+def main(path, top=8):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr = rows[0]
+    res = []
+    for r in rows[2:]:
+        name = r[hdr.index("Kernel Name")]
+        print(name[:110])
+        d = {}
+        for k in KEYS:
+            if k in hdr:
+                d[k] = r[hdr.index(k)]
+                print(f"   {k:70s} {r[hdr.index(k)]}")
+        st = [(hdr[i], r[i]) for i in range(len(hdr))
+              if "warp_issue_stalled" in hdr[i] and hdr[i].endswith("per_warp_active.pct") and r[i]]
+        st = sorted(st, key=lambda x: -float(x[1]))[:top]
+        for s in st:
+            print(f"      stall {s[0].replace('smsp__warp_issue_stalled_', ''):55s} {s[1]}")
+        res.append((name, d))
+    return res
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
