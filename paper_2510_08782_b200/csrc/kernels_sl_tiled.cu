@@ -113,6 +113,13 @@ __global__ void __launch_bounds__(256) k_sl_tiled(Geom g, int ZC, TileArgs a) {
 
   double acc = 0.0, vs0 = 0.0, vs1 = 0.0, vs2 = 0.0;
   int slot0 = 0;  // ring slot of plane z - HALO
+  // per-point streams of the current plane, prefetched one plane ahead (hides HBM latency)
+  const size_t gi0 = (size_t)z0 * plane + (size_t)(y0 + ty) * g.nx + x0 + tx;
+  float nd0 = 0.f, nd1 = 0.f, nd2 = 0.f, nE = 1.f;
+  if (MODE != M_TRACE) {
+    nd0 = __ldg(a.delta + gi0); nd1 = __ldg(a.delta + F + gi0); nd2 = __ldg(a.delta + 2 * F + gi0);
+    if (HAS_E) nE = __ldg(a.E + gi0);
+  }
 #pragma unroll 1
   for (int zi = 0; zi < ZC; ++zi) {
     const int z = z0 + zi;
@@ -124,7 +131,13 @@ __global__ void __launch_bounds__(256) k_sl_tiled(Geom g, int ZC, TileArgs a) {
       for (int f = 0; f < NF; ++f) pre[f] = __ldg(reinterpret_cast<const float4*>(a.in[f] + po));
     }
     const int x = x0 + tx, y = y0 + ty;
-    const size_t gi = (size_t)z * plane + (size_t)y * g.nx + x;
+    const size_t gi = gi0 + (size_t)zi * plane;
+    const float cd0 = nd0, cd1 = nd1, cd2 = nd2, cE = nE;
+    if (MODE != M_TRACE && zi + 1 < ZC) {
+      const size_t gn = gi + plane;
+      nd0 = __ldg(a.delta + gn); nd1 = __ldg(a.delta + F + gn); nd2 = __ldg(a.delta + 2 * F + gn);
+      if (HAS_E) nE = __ldg(a.E + gn);
+    }
 
     // gather NF fields at l + (dx, dy, dz) from the smem ring (or global fallback)
     auto gather = [&](float dx, float dy, float dz, float* res) {
@@ -185,15 +198,14 @@ __global__ void __launch_bounds__(256) k_sl_tiled(Geom g, int ZC, TileArgs a) {
         o[2 * F + gi] = sg * g.cz * r[2];
       }
     } else {
-      const float dx = a.delta[gi], dy = a.delta[F + gi], dz = a.delta[2 * F + gi];
       float r[NF];
-      gather(dx, dy, dz, r);
+      gather(cd0, cd1, cd2, r);
       if (MODE == M_EFACTOR) {
         const float bv = sm[((slot0 + HALO) % NZR) * PS + (ty + HALO) * PW + tx + XH];  // divv(l)
         a.out[0][gi] = 1.0f + a.sh * (r[0] + bv) + a.h2 * r[0] * bv;
       } else {
         float val = r[0];
-        if (HAS_E) val *= a.E[gi];
+        if (HAS_E) val *= cE;
         a.out[0][gi] = val;
         if (MODE == M_LAST) {
           const float res = a.m1[gi] - val;
@@ -248,7 +260,7 @@ bool tiled_ok(const Geom& g) {
   return g.d == 3 && g.nx >= tiled::TX && g.nx % tiled::TX == 0 && g.ny % tiled::TY == 0 && g.nz >= 8;
 }
 
-static int tiled_zc(const Geom& g) { return g.nz < 32 ? g.nz : 32; }
+static int tiled_zc(const Geom& g) { return g.nz < 64 ? g.nz : 64; }
 
 int tiled_blocks(const Geom& g) { return (g.nx / tiled::TX) * (g.ny / tiled::TY) * (g.nz / tiled_zc(g)); }
 
