@@ -79,22 +79,28 @@ def test_precond_and_leray(cfg, n, model):
 @pytest.mark.parametrize("cfg,n", GRIDS)
 @pytest.mark.parametrize("model", [0, 1, 2])
 def test_eval_gradient(cfg, n, model):
+    """Whole evaluation.  The adjoint starts from the mismatch lam^S = m1 - m^S (R1), whose relative
+    error is the forward sweep's (<= 1e-5 of ||m^S||) times kappa = ||m^S|| / ||m1 - m^S||; lam, b
+    and g are therefore held to TOL * max(1, kappa), everything else to TOL."""
     d = case(cfg, n, model=model)
     if model == 2:
         d["v"] = spectral.leray(d["grid"], d["v"]).astype(np.float32).astype(np.float64)
     t = topt_for(d)
     g, s, sc = t.eval_gradient(dev(d["m0"]), dev(d["m1"]), dev(d["v"]))
     ref = ogr.evaluate(d["prob"], d["v"])
+    kappa = max(1.0, np.linalg.norm(ref["m"][-1]) / np.linalg.norm(ref["lam"][-1]))
+    tol_adj = TOL * kappa
     lam, b = t.adjoint()
     lam, b = host(lam), host(b)
     for j in range(d["nt"] + 1):
-        assert rel_l2(lam[j], ref["lam"][j]) < TOL, ("lam", j)
-    assert rel_l2(b, ref["b"]) < TOL, "b"
-    assert rel_l2(host(g), ref["g"]) < TOL, "g"
+        assert rel_l2(lam[j], ref["lam"][j]) < tol_adj, ("lam", j)
+    assert rel_l2(b, ref["b"]) < tol_adj, "b"
+    assert rel_l2(host(g), ref["g"]) < tol_adj, "g"
     assert rel_l2(host(s), ref["s"]) < TOL, "s"
     sd = t.scalars_dict(sc)
-    for k in ("obj", "dist", "reg", "grad_inf", "gs"):
+    for k in ("obj", "dist", "reg", "gs"):
         assert abs(sd[k] - ref[k]) <= TOL * abs(ref[k]) + 1e-30, k
+    assert abs(sd["grad_inf"] - ref["grad_inf"]) <= tol_adj * ref["grad_inf"]
 
 
 def test_multidot_and_mix():
