@@ -46,6 +46,10 @@ struct LineCfg {
   static constexpr int STRIDE = fft_line_stride(N);  // complex elements per smem line
 };
 
+// max radix per element type: fp64 lines use radix 8 (half the registers / smem per thread)
+template <typename C> struct RM { static constexpr int v = 16; };
+template <> struct RM<double2> { static constexpr int v = 8; };
+
 __device__ __forceinline__ int paired_pos(int q, int N) {  // natural index -> paired position
   return q == 0 ? 0 : (q == N / 2 ? 1 : (q < N / 2 ? 2 * q : 2 * (N - q) + 1));
 }
@@ -300,7 +304,7 @@ struct RealIn { const float* re[3]; const float* im[3]; };
 // x pass forward: Z_f[row][q] = FFT_x(re_f + i im_f)[q]
 template <int N, typename C>
 __global__ void __launch_bounds__(kThreads) k_px_fwd(Geom g, RealIn in, ZList<C> Z) {
-  using L = LineCfg<N>;
+  using L = LineCfg<N, RM<C>::v>;
   using T = typename Real<C>::T;
   extern __shared__ __align__(16) unsigned char smraw[];
   C* buf = reinterpret_cast<C*>(smraw);
@@ -329,7 +333,7 @@ __global__ void __launch_bounds__(kThreads) k_px_fwd(Geom g, RealIn in, ZList<C>
   }
   __syncthreads();
   const int myline = threadIdx.x / L::T, tid = threadIdx.x % L::T;
-  fft_line<N, false>(buf + myline * L::STRIDE, tw, tid, myline < L::LPB);
+  fft_line<N, false, RM<C>::v>(buf + myline * L::STRIDE, tw, tid, myline < L::LPB);
   for (int i = threadIdx.x; i < L::LPB * N; i += kThreads) {
     const int rl = i / N, q = i % N;
     if (row0 + rl < nrows) Zf[(row0 + rl) * N + q] = buf[rl * L::STRIDE + fft_pad(q)];
@@ -340,7 +344,7 @@ __global__ void __launch_bounds__(kThreads) k_px_fwd(Geom g, RealIn in, ZList<C>
 struct RealOut { float* re[3]; float* im[3]; };
 template <int N, typename C>
 __global__ void __launch_bounds__(kThreads) k_px_inv(Geom g, ZList<C> Z, RealOut out) {
-  using L = LineCfg<N>;
+  using L = LineCfg<N, RM<C>::v>;
   extern __shared__ __align__(16) unsigned char smraw[];
   C* buf = reinterpret_cast<C*>(smraw);
   C* tw = buf + L::LPB * L::STRIDE;
@@ -357,7 +361,7 @@ __global__ void __launch_bounds__(kThreads) k_px_inv(Geom g, ZList<C> Z, RealOut
   }
   __syncthreads();
   const int myline = threadIdx.x / L::T, tid = threadIdx.x % L::T;
-  fft_line<N, true>(buf + myline * L::STRIDE, tw, tid, myline < L::LPB);
+  fft_line<N, true, RM<C>::v>(buf + myline * L::STRIDE, tw, tid, myline < L::LPB);
   float* re = out.re[f];
   float* im = out.im[f];
   const int n4 = L::LPB * N / 4;
@@ -392,7 +396,7 @@ __device__ __forceinline__ double regL(double kk, int p) { return p == 1 ? kk : 
 template <int N, int MODE, typename C>
 __global__ void __launch_bounds__(kThreads) k_pstrided(Geom g, int axis, int TXC, int NIN, int NOUT, ZList<C> Z,
                                                        SpecOp op) {
-  using L = LineCfg<N>;
+  using L = LineCfg<N, RM<C>::v>;
   using T = typename Real<C>::T;
   extern __shared__ __align__(16) unsigned char smraw[];
   C* buf = reinterpret_cast<C*>(smraw);
@@ -414,7 +418,7 @@ __global__ void __launch_bounds__(kThreads) k_pstrided(Geom g, int axis, int TXC
   }
   __syncthreads();
   const int myline = threadIdx.x / L::T, tid = threadIdx.x % L::T;
-  if (MODE != 1) fft_line<N, false>(buf + myline * L::STRIDE, tw, tid, myline < nin);
+  if (MODE != 1) fft_line<N, false, RM<C>::v>(buf + myline * L::STRIDE, tw, tid, myline < nin);
   if (MODE >= 2) {
     for (int i = threadIdx.x; i < N * TXC; i += blockDim.x) {
       const int q = i / TXC, c = i % TXC;
@@ -432,9 +436,11 @@ __global__ void __launch_bounds__(kThreads) k_pstrided(Geom g, int axis, int TXC
       const double Lk = regL(kx * kx + ky * ky + kz * kz, op.p);
       const double Lt = Lk == 0.0 ? 1.0 : Lk;  // kernel fix
       if (MODE == 2 || MODE == 3) {
-        const double m = MODE == 2 ? op.alpha * Lk * op.invn : -op.invn / (op.alpha * Lt);
+        // fp32 chain: the smoothing multiplier in float (relative 1e-7), no fp64 division
+        const T m = MODE == 2 ? (T)(op.alpha * Lk * op.invn)
+                              : (T)(-(float)op.invn * __frcp_rn((float)(op.alpha * Lt)));
         C& z = buf[c * L::STRIDE + fft_pad(q)];
-        z = mk((T)(z.x * m), (T)(z.y * m));
+        z = mk(z.x * m, z.y * m);
       } else {
         // Leray on the d components at this k (Nyquist-zeroed k', R3/R9)
         const double kp2 = kxp * kxp + kyp * kyp + kzp * kzp;
@@ -445,14 +451,18 @@ __global__ void __launch_bounds__(kThreads) k_pstrided(Geom g, int axis, int TXC
           bx[f] = z.x; by[f] = z.y;
         }
         if (kp2 > 0.0) {
+          // per-mode relative precision suffices here (a 0-order projector), so fp32 reciprocal
+          const double ikp = (double)__frcp_rn((float)kp2);
           double dx = 0.0, dy = 0.0;
           for (int f = 0; f < NIN; ++f) { dx += kp[f] * bx[f]; dy += kp[f] * by[f]; }
-          for (int f = 0; f < NIN; ++f) { bx[f] -= kp[f] * dx / kp2; by[f] -= kp[f] * dy / kp2; }
+          dx *= ikp;
+          dy *= ikp;
+          for (int f = 0; f < NIN; ++f) { bx[f] -= kp[f] * dx; by[f] -= kp[f] * dy; }
         }
         // each component's spectrum is bx + i by; pack pairs of REAL fields: A + i B has
         // spectrum A^ + i B^ = (Ax - By) + i (Ay + Bx)
         const double sl = MODE == 5 ? op.alpha * Lk * op.invn : op.invn;
-        const double sp = -op.invn / (op.alpha * Lt);
+        const double sp = -op.invn * (double)__frcp_rn((float)(op.alpha * Lt));
         auto put = [&](int slot, int a, int b, double sa, double sb) {
           const double ax = a >= 0 ? sa * bx[a] : 0.0, ay = a >= 0 ? sa * by[a] : 0.0;
           const double cx = b >= 0 ? sb * bx[b] : 0.0, cy = b >= 0 ? sb * by[b] : 0.0;
@@ -471,7 +481,7 @@ __global__ void __launch_bounds__(kThreads) k_pstrided(Geom g, int axis, int TXC
     __syncthreads();
   }
   const int nout = NOUT * TXC;
-  if (MODE != 0) fft_line<N, true>(buf + myline * L::STRIDE, tw, tid, myline < nout);
+  if (MODE != 0) fft_line<N, true, RM<C>::v>(buf + myline * L::STRIDE, tw, tid, myline < nout);
   for (int i = threadIdx.x; i < N * nout; i += blockDim.x) {
     const int row = i / nout, l = i % nout;
     const int f = f0 + l / TXC, c = l % TXC;
@@ -516,34 +526,39 @@ __global__ void __launch_bounds__(kThreads) k_assemble(Geom g, int RB, int lpr, 
   fft_line<N, true>(buf + myline * L::STRIDE, tw, tid, myline < nlines);
   double gmax = 0.0, sgs = 0.0, svu = 0.0, ssu = 0.0, sg[3] = {0, 0, 0}, ss[3] = {0, 0, 0};
   const double nF = (double)g.F;
-  for (int i = threadIdx.x; i < RB * N; i += blockDim.x) {
-    const int r = i / N, x = i % N;
+  const int pf = leray ? lpr / 2 : 0;  // first p field
+  for (int i4 = threadIdx.x; i4 < RB * N / 4; i4 += blockDim.x) {
+    const int r = (4 * i4) / N, x = (4 * i4) % N;
     if (row0 + r >= nrows) continue;
     const size_t gi = (row0 + r) * N + x;
-    const int pf = leray ? lpr / 2 : 0;  // first p field
     for (int c = 0; c < g.d; ++c) {
-      float bl, pc;
-      const float2 wp = buf[(r * lpr + pf + c / 2) * L::STRIDE + fft_pad(x)];
-      pc = (c & 1) ? wp.y : wp.x;
-      if (leray) {
-        const float2 wb = buf[(r * lpr + c / 2) * L::STRIDE + fft_pad(x)];
-        bl = (c & 1) ? wb.y : wb.x;
-      } else {
-        bl = a.b ? a.b[c * g.F + gi] : 0.f;
+      const size_t o = c * g.F + gi;
+      float4 bl, pc;
+      {
+        const float2* L = buf + (r * lpr + pf + c / 2) * L::STRIDE;
+        const float2 w0 = L[fft_pad(x)], w1 = L[fft_pad(x + 1)], w2 = L[fft_pad(x + 2)], w3 = L[fft_pad(x + 3)];
+        pc = (c & 1) ? make_float4(w0.y, w1.y, w2.y, w3.y) : make_float4(w0.x, w1.x, w2.x, w3.x);
       }
-      const float uc = a.u ? a.u[c * g.F + gi] : 0.f;
-      const float vc = a.v ? a.v[c * g.F + gi] : 0.f;
+      if (leray) {
+        const float2* L = buf + (r * lpr + c / 2) * L::STRIDE;
+        const float2 w0 = L[fft_pad(x)], w1 = L[fft_pad(x + 1)], w2 = L[fft_pad(x + 2)], w3 = L[fft_pad(x + 3)];
+        bl = (c & 1) ? make_float4(w0.y, w1.y, w2.y, w3.y) : make_float4(w0.x, w1.x, w2.x, w3.x);
+      } else {
+        bl = a.b ? __ldg(reinterpret_cast<const float4*>(a.b + o)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      const float4 uc = a.u ? __ldg(reinterpret_cast<const float4*>(a.u + o)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 vc = a.v ? __ldg(reinterpret_cast<const float4*>(a.v + o)) : make_float4(0.f, 0.f, 0.f, 0.f);
       const float vbar = a.vsum ? (float)(a.vsum[c] / nF) : 0.f;
-      const float gv = uc + bl;
-      const float sv = -(vc - vbar) + pc;
-      if (a.g) a.g[c * g.F + gi] = gv;
-      if (a.s) a.s[c * g.F + gi] = sv;
-      gmax = fmax(gmax, (double)fabsf(gv));
-      sgs += (double)gv * (double)sv;
-      svu += (double)vc * (double)uc;
-      ssu += (double)sv * (double)uc;
-      sg[c] += (double)gv;
-      ss[c] += (double)sv;
+      const float4 gv = make_float4(uc.x + bl.x, uc.y + bl.y, uc.z + bl.z, uc.w + bl.w);
+      const float4 sv = make_float4(vbar - vc.x + pc.x, vbar - vc.y + pc.y, vbar - vc.z + pc.z, vbar - vc.w + pc.w);
+      if (a.g) *reinterpret_cast<float4*>(a.g + o) = gv;
+      if (a.s) *reinterpret_cast<float4*>(a.s + o) = sv;
+      gmax = fmax(gmax, (double)fmaxf(fmaxf(fabsf(gv.x), fabsf(gv.y)), fmaxf(fabsf(gv.z), fabsf(gv.w))));
+      sgs += (double)(gv.x * sv.x) + (double)(gv.y * sv.y) + (double)(gv.z * sv.z) + (double)(gv.w * sv.w);
+      svu += (double)vc.x * uc.x + (double)vc.y * uc.y + (double)vc.z * uc.z + (double)vc.w * uc.w;
+      ssu += (double)sv.x * uc.x + (double)sv.y * uc.y + (double)sv.z * uc.z + (double)sv.w * uc.w;
+      sg[c] += (double)gv.x + (double)gv.y + (double)gv.z + (double)gv.w;
+      ss[c] += (double)sv.x + (double)sv.y + (double)sv.z + (double)sv.w;
     }
   }
   double vals[10] = {gmax, sgs, svu, ssu, sg[0], sg[1], sg[2], ss[0], ss[1], ss[2]};
@@ -570,12 +585,12 @@ __global__ void __launch_bounds__(kThreads) k_assemble(Geom g, int RB, int lpr, 
 
 template <int N, typename C>
 static size_t smem_lines(int nlines) {
-  return (size_t)(nlines * LineCfg<N>::STRIDE + N) * sizeof(C);
+  return (size_t)(nlines * LineCfg<N, RM<C>::v>::STRIDE + N) * sizeof(C);
 }
 
 template <int N, typename C>
 static void px_fwd_launch(const Geom& g, const RealIn& in, const ZList<C>& Z, int nf, cudaStream_t st) {
-  using L = LineCfg<N>;
+  using L = LineCfg<N, RM<C>::v>;
   const size_t sm = smem_lines<N, C>(L::LPB);
   const size_t nrows = (size_t)g.ny * g.nz;
   dim3 grid((unsigned)((nrows + L::LPB - 1) / L::LPB), nf);
@@ -586,7 +601,7 @@ static void px_fwd_launch(const Geom& g, const RealIn& in, const ZList<C>& Z, in
 
 template <int N, typename C>
 static void px_inv_launch(const Geom& g, const ZList<C>& Z, const RealOut& out, int nf, cudaStream_t st) {
-  using L = LineCfg<N>;
+  using L = LineCfg<N, RM<C>::v>;
   const size_t sm = smem_lines<N, C>(L::LPB);
   const size_t nrows = (size_t)g.ny * g.nz;
   dim3 grid((unsigned)((nrows + L::LPB - 1) / L::LPB), nf);
@@ -598,7 +613,7 @@ static void px_inv_launch(const Geom& g, const ZList<C>& Z, const RealOut& out, 
 template <int N, int MODE, typename C>
 static void pstrided_launch(const Geom& g, int axis, const ZList<C>& Z, int nin, int nout, const SpecOp& op,
                             cudaStream_t st) {
-  using L = LineCfg<N>;
+  using L = LineCfg<N, RM<C>::v>;
   const bool multi = MODE >= 4;
   const int NIN = multi ? nin : 1, NOUT = multi ? nout : 1;
   const int NL = NIN > NOUT ? NIN : NOUT;
