@@ -411,17 +411,22 @@ __global__ void __launch_bounds__(kThreads) k_pstrided(Geom g, int axis, int TXC
   if (axis == 1) { base = ((size_t)outer << (g.lx + g.ly)) + x0; S = g.nx; }
   else { base = ((size_t)outer << g.lx) + x0; S = (size_t)g.nx * g.ny; }
   const int nin = NIN * TXC;
-  for (int i = threadIdx.x; i < N * nin; i += blockDim.x) {
-    const int row = i / nin, l = i % nin;
-    const int f = f0 + l / TXC, c = l % TXC;
-    buf[l * L::STRIDE + fft_pad(row)] = Z.z[f][base + row * S + c];
+  const int ltx = __ffs(TXC) - 1;  // TXC is a power of two
+  const unsigned bs = (unsigned)base, Su = (unsigned)S;
+  for (int f = 0; f < NIN; ++f) {
+    const C* __restrict__ src = Z.z[f0 + f];
+    C* dst = buf + f * TXC * L::STRIDE;
+    for (int i = threadIdx.x; i < N * TXC; i += blockDim.x) {
+      const int row = i >> ltx, c = i & (TXC - 1);
+      dst[c * L::STRIDE + fft_pad(row)] = src[bs + row * Su + c];
+    }
   }
   __syncthreads();
   const int myline = threadIdx.x / L::T, tid = threadIdx.x % L::T;
   if (MODE != 1) fft_line<N, false, RM<C>::v>(buf + myline * L::STRIDE, tw, tid, myline < nin);
   if (MODE >= 2) {
     for (int i = threadIdx.x; i < N * TXC; i += blockDim.x) {
-      const int q = i / TXC, c = i % TXC;
+      const int q = i >> ltx, c = i & (TXC - 1);
       const int qx = x0 + c;
       const double kx = qx <= g.nx / 2 ? qx : qx - g.nx, kxp = qx == g.nx / 2 ? 0.0 : kx;
       double ky, kyp, kz, kzp;
@@ -482,10 +487,13 @@ __global__ void __launch_bounds__(kThreads) k_pstrided(Geom g, int axis, int TXC
   }
   const int nout = NOUT * TXC;
   if (MODE != 0) fft_line<N, true, RM<C>::v>(buf + myline * L::STRIDE, tw, tid, myline < nout);
-  for (int i = threadIdx.x; i < N * nout; i += blockDim.x) {
-    const int row = i / nout, l = i % nout;
-    const int f = f0 + l / TXC, c = l % TXC;
-    Z.z[f][base + row * S + c] = buf[l * L::STRIDE + fft_pad(row)];
+  for (int f = 0; f < NOUT; ++f) {
+    C* __restrict__ dst = Z.z[f0 + f];
+    const C* src = buf + f * TXC * L::STRIDE;
+    for (int i = threadIdx.x; i < N * TXC; i += blockDim.x) {
+      const int row = i >> ltx, c = i & (TXC - 1);
+      dst[bs + row * Su + c] = src[c * L::STRIDE + fft_pad(row)];
+    }
   }
 }
 
@@ -516,7 +524,7 @@ __global__ void __launch_bounds__(kThreads) k_assemble(Geom g, int RB, int lpr, 
   const int nlines = RB * lpr;
   for (int i = threadIdx.x; i < nlines * N; i += blockDim.x) {
     const int l = i / N, q = i % N;
-    const int r = l / lpr, f = l % lpr;
+    const int r = l >> (lpr >> 1), f = l & (lpr - 1);  // lpr in {1, 2, 4}
     float2 z = make_float2(0.f, 0.f);
     if (row0 + r < nrows) z = a.Z[f][(row0 + r) * N + q];
     buf[l * L::STRIDE + fft_pad(q)] = z;
