@@ -393,108 +393,151 @@ struct SpecOp {
 
 __device__ __forceinline__ double regL(double kk, int p) { return p == 1 ? kk : (p == 2 ? kk * kk : kk * kk * kk); }
 
+// cp.async (LDGSTS) helpers: global -> shared copies that bypass registers
+__device__ __forceinline__ void cp_async(void* smem, const float2* g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(g));
+}
+__device__ __forceinline__ void cp_async(void* smem, const double2* g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_wait_0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+// Persistent and double-buffered: a block walks work items (tile x field); the tile of
+// item k+1 is copied global -> shared with cp.async while item k is transformed, so HBM
+// latency overlaps the FFT instead of stalling every block at a barrier.
 template <int N, int MODE, typename C>
 __global__ void __launch_bounds__(kThreads) k_pstrided(Geom g, int axis, int TXC, int NIN, int NOUT, ZList<C> Z,
-                                                       SpecOp op) {
+                                                       SpecOp op, int nitems) {
   using L = LineCfg<N, RM<C>::v>;
   using T = typename Real<C>::T;
   extern __shared__ __align__(16) unsigned char smraw[];
-  C* buf = reinterpret_cast<C*>(smraw);
   const int NL = NIN > NOUT ? NIN : NOUT;  // line slots per column
-  C* tw = buf + NL * TXC * L::STRIDE;
+  const int lines = NL * TXC;
+  C* buf0 = reinterpret_cast<C*>(smraw);
+  C* buf1 = buf0 + lines * L::STRIDE;
+  C* tw = buf1 + lines * L::STRIDE;
   load_twiddles<N>(tw);
   const int tilesx = g.nx / TXC;
-  const int x0 = (blockIdx.x % tilesx) * TXC;
-  const int outer = blockIdx.x / tilesx;           // z (axis y) or y (axis z)
-  const int f0 = (MODE >= 4) ? 0 : blockIdx.y;     // field of this block (Leray modes: all fields)
-  size_t base, S;
-  if (axis == 1) { base = ((size_t)outer << (g.lx + g.ly)) + x0; S = g.nx; }
-  else { base = ((size_t)outer << g.lx) + x0; S = (size_t)g.nx * g.ny; }
-  const int nin = NIN * TXC;
+  const int outerN = axis == 1 ? g.nz : g.ny;
+  const int tiles = tilesx * outerN;
   const int ltx = __ffs(TXC) - 1;  // TXC is a power of two
-  const unsigned bs = (unsigned)base, Su = (unsigned)S;
-  for (int f = 0; f < NIN; ++f) {
-    const C* __restrict__ src = Z.z[f0 + f];
-    C* dst = buf + f * TXC * L::STRIDE;
-    for (int i = threadIdx.x; i < N * TXC; i += blockDim.x) {
-      const int row = i >> ltx, c = i & (TXC - 1);
-      dst[c * L::STRIDE + fft_pad(row)] = src[bs + row * Su + c];
-    }
-  }
-  __syncthreads();
+  const unsigned Su = axis == 1 ? (unsigned)g.nx : (unsigned)g.nx * g.ny;
+  const int nin = NIN * TXC, nout = NOUT * TXC;
   const int myline = threadIdx.x / L::T, tid = threadIdx.x % L::T;
-  if (MODE != 1) fft_line<N, false, RM<C>::v>(buf + myline * L::STRIDE, tw, tid, myline < nin);
-  if (MODE >= 2) {
-    for (int i = threadIdx.x; i < N * TXC; i += blockDim.x) {
-      const int q = i >> ltx, c = i & (TXC - 1);
-      const int qx = x0 + c;
-      const double kx = qx <= g.nx / 2 ? qx : qx - g.nx, kxp = qx == g.nx / 2 ? 0.0 : kx;
-      double ky, kyp, kz, kzp;
-      if (g.d == 3) {
-        const int qy = outer;
-        ky = qy <= g.ny / 2 ? qy : qy - g.ny; kyp = qy == g.ny / 2 ? 0.0 : ky;
-        kz = q <= N / 2 ? q : q - N; kzp = q == N / 2 ? 0.0 : kz;
-      } else {
-        ky = q <= N / 2 ? q : q - N; kyp = q == N / 2 ? 0.0 : ky;
-        kz = 0.0; kzp = 0.0;
-      }
-      const double Lk = regL(kx * kx + ky * ky + kz * kz, op.p);
-      const double Lt = Lk == 0.0 ? 1.0 : Lk;  // kernel fix
-      if (MODE == 2 || MODE == 3) {
-        // fp32 chain: the smoothing multiplier in float (relative 1e-7), no fp64 division
-        const T m = MODE == 2 ? (T)(op.alpha * Lk * op.invn)
-                              : (T)(-(float)op.invn * __frcp_rn((float)(op.alpha * Lt)));
-        C& z = buf[c * L::STRIDE + fft_pad(q)];
-        z = mk(z.x * m, z.y * m);
-      } else {
-        // Leray on the d components at this k (Nyquist-zeroed k', R3/R9)
-        const double kp2 = kxp * kxp + kyp * kyp + kzp * kzp;
-        const double kp[3] = {kxp, kyp, kzp};
-        double bx[3] = {0, 0, 0}, by[3] = {0, 0, 0};
-        for (int f = 0; f < NIN; ++f) {
-          const C z = buf[(f * TXC + c) * L::STRIDE + fft_pad(q)];
-          bx[f] = z.x; by[f] = z.y;
-        }
-        if (kp2 > 0.0) {
-          // per-mode relative precision suffices here (a 0-order projector), so fp32 reciprocal
-          const double ikp = (double)__frcp_rn((float)kp2);
-          double dx = 0.0, dy = 0.0;
-          for (int f = 0; f < NIN; ++f) { dx += kp[f] * bx[f]; dy += kp[f] * by[f]; }
-          dx *= ikp;
-          dy *= ikp;
-          for (int f = 0; f < NIN; ++f) { bx[f] -= kp[f] * dx; by[f] -= kp[f] * dy; }
-        }
-        // each component's spectrum is bx + i by; pack pairs of REAL fields: A + i B has
-        // spectrum A^ + i B^ = (Ax - By) + i (Ay + Bx)
-        const double sl = MODE == 5 ? op.alpha * Lk * op.invn : op.invn;
-        const double sp = -op.invn * (double)__frcp_rn((float)(op.alpha * Lt));
-        auto put = [&](int slot, int a, int b, double sa, double sb) {
-          const double ax = a >= 0 ? sa * bx[a] : 0.0, ay = a >= 0 ? sa * by[a] : 0.0;
-          const double cx = b >= 0 ? sb * bx[b] : 0.0, cy = b >= 0 ? sb * by[b] : 0.0;
-          buf[(slot * TXC + c) * L::STRIDE + fft_pad(q)] = mk((T)(ax - cy), (T)(ay + cx));
-        };
-        if (g.d == 3) {
-          put(0, 0, 1, sl, sl);
-          put(1, 2, -1, sl, 0.0);
-          if (MODE == 4) { put(2, 0, 1, sp, sp); put(3, 2, -1, sp, 0.0); }
-        } else {
-          put(0, 0, 1, sl, sl);
-          if (MODE == 4) put(1, 0, 1, sp, sp);
-        }
+
+  auto item_geom = [&](int item, int& f0, int& x0, int& outer, unsigned& base) {
+    const int t = item % tiles;
+    f0 = (MODE >= 4) ? 0 : item / tiles;
+    x0 = (t % tilesx) * TXC;
+    outer = t / tilesx;
+    base = axis == 1 ? ((unsigned)outer << (g.lx + g.ly)) + x0 : ((unsigned)outer << g.lx) + x0;
+  };
+  auto prefetch = [&](int item, C* buf) {
+    int f0, x0, outer;
+    unsigned base;
+    item_geom(item, f0, x0, outer, base);
+    for (int f = 0; f < NIN; ++f) {
+      const C* __restrict__ src = Z.z[f0 + f];
+      C* dst = buf + f * TXC * L::STRIDE;
+      for (int i = threadIdx.x; i < N * TXC; i += blockDim.x) {
+        const int row = i >> ltx, c = i & (TXC - 1);
+        cp_async(dst + c * L::STRIDE + fft_pad(row), src + base + row * Su + c);
       }
     }
+  };
+
+  int item = blockIdx.x;
+  bool cur0 = true;
+  if (item < nitems) prefetch(item, buf0);
+  cp_commit();
+  for (; item < nitems; item += gridDim.x, cur0 = !cur0) {
+    C* buf = cur0 ? buf0 : buf1;
+    const int next = item + gridDim.x;
+    if (next < nitems) prefetch(next, cur0 ? buf1 : buf0);
+    cp_commit();
+    cp_wait_1();  // this item's copies have landed (the next item's may still be in flight)
     __syncthreads();
-  }
-  const int nout = NOUT * TXC;
-  if (MODE != 0) fft_line<N, true, RM<C>::v>(buf + myline * L::STRIDE, tw, tid, myline < nout);
-  for (int f = 0; f < NOUT; ++f) {
-    C* __restrict__ dst = Z.z[f0 + f];
-    const C* src = buf + f * TXC * L::STRIDE;
-    for (int i = threadIdx.x; i < N * TXC; i += blockDim.x) {
-      const int row = i >> ltx, c = i & (TXC - 1);
-      dst[bs + row * Su + c] = src[c * L::STRIDE + fft_pad(row)];
+    int f0, x0, outer;
+    unsigned base;
+    item_geom(item, f0, x0, outer, base);
+    if (MODE != 1) fft_line<N, false, RM<C>::v>(buf + myline * L::STRIDE, tw, tid, myline < nin);
+    if (MODE >= 2) {
+      for (int i = threadIdx.x; i < N * TXC; i += blockDim.x) {
+        const int q = i >> ltx, c = i & (TXC - 1);
+        const int qx = x0 + c;
+        const double kx = qx <= g.nx / 2 ? qx : qx - g.nx, kxp = qx == g.nx / 2 ? 0.0 : kx;
+        double ky, kyp, kz, kzp;
+        if (g.d == 3) {
+          const int qy = outer;
+          ky = qy <= g.ny / 2 ? qy : qy - g.ny; kyp = qy == g.ny / 2 ? 0.0 : ky;
+          kz = q <= N / 2 ? q : q - N; kzp = q == N / 2 ? 0.0 : kz;
+        } else {
+          ky = q <= N / 2 ? q : q - N; kyp = q == N / 2 ? 0.0 : ky;
+          kz = 0.0; kzp = 0.0;
+        }
+        const double Lk = regL(kx * kx + ky * ky + kz * kz, op.p);
+        const double Lt = Lk == 0.0 ? 1.0 : Lk;  // kernel fix
+        if (MODE == 2 || MODE == 3) {
+          // the smoothing multiplier in float (relative 1e-7); no fp64 division
+          const T m = MODE == 2 ? (T)(op.alpha * Lk * op.invn)
+                                : (T)(-(float)op.invn * __frcp_rn((float)(op.alpha * Lt)));
+          C& z = buf[c * L::STRIDE + fft_pad(q)];
+          z = mk(z.x * m, z.y * m);
+        } else {
+          // Leray on the d components at this k (Nyquist-zeroed k', R3/R9)
+          const double kp2 = kxp * kxp + kyp * kyp + kzp * kzp;
+          const double kp[3] = {kxp, kyp, kzp};
+          double bx[3] = {0, 0, 0}, by[3] = {0, 0, 0};
+          for (int f = 0; f < NIN; ++f) {
+            const C z = buf[(f * TXC + c) * L::STRIDE + fft_pad(q)];
+            bx[f] = z.x; by[f] = z.y;
+          }
+          if (kp2 > 0.0) {
+            // per-mode relative precision suffices (a 0-order projector): fp32 reciprocal
+            const double ikp = (double)__frcp_rn((float)kp2);
+            double dx = 0.0, dy = 0.0;
+            for (int f = 0; f < NIN; ++f) { dx += kp[f] * bx[f]; dy += kp[f] * by[f]; }
+            dx *= ikp;
+            dy *= ikp;
+            for (int f = 0; f < NIN; ++f) { bx[f] -= kp[f] * dx; by[f] -= kp[f] * dy; }
+          }
+          // each component's spectrum is bx + i by; pack pairs of REAL fields: A + i B has
+          // spectrum A^ + i B^ = (Ax - By) + i (Ay + Bx)
+          const double sl = MODE == 5 ? op.alpha * Lk * op.invn : op.invn;
+          const double sp = -op.invn * (double)__frcp_rn((float)(op.alpha * Lt));
+          auto put = [&](int slot, int a, int b, double sa, double sb) {
+            const double ax = a >= 0 ? sa * bx[a] : 0.0, ay = a >= 0 ? sa * by[a] : 0.0;
+            const double cx = b >= 0 ? sb * bx[b] : 0.0, cy = b >= 0 ? sb * by[b] : 0.0;
+            buf[(slot * TXC + c) * L::STRIDE + fft_pad(q)] = mk((T)(ax - cy), (T)(ay + cx));
+          };
+          if (g.d == 3) {
+            put(0, 0, 1, sl, sl);
+            put(1, 2, -1, sl, 0.0);
+            if (MODE == 4) { put(2, 0, 1, sp, sp); put(3, 2, -1, sp, 0.0); }
+          } else {
+            put(0, 0, 1, sl, sl);
+            if (MODE == 4) put(1, 0, 1, sp, sp);
+          }
+        }
+      }
+      __syncthreads();
     }
+    if (MODE != 0) fft_line<N, true, RM<C>::v>(buf + myline * L::STRIDE, tw, tid, myline < nout);
+    for (int f = 0; f < NOUT; ++f) {
+      C* __restrict__ dst = Z.z[f0 + f];
+      const C* src = buf + f * TXC * L::STRIDE;
+      for (int i = threadIdx.x; i < N * TXC; i += blockDim.x) {
+        const int row = i >> ltx, c = i & (TXC - 1);
+        dst[base + row * Su + c] = src[c * L::STRIDE + fft_pad(row)];
+      }
+    }
+    __syncthreads();  // this buffer is refilled by the prefetch issued at the next iteration
   }
+  cp_wait_0();
 }
 
 // Assembly (x^-1 of the b-chain + pointwise combine), per x row (R9):
@@ -631,12 +674,19 @@ static void pstrided_launch(const Geom& g, int axis, const ZList<C>& Z, int nin,
   TXC = t;
   if (TXC > g.nx) TXC = g.nx;
   if (TXC < 1) TXC = 1;
-  const size_t sm = smem_lines<N, C>(NL * TXC);
+  const size_t sm = (size_t)(2 * NL * TXC * L::STRIDE + N) * sizeof(C);
   const int outer = axis == 1 ? g.nz : g.ny;
-  dim3 grid((g.nx / TXC) * outer, multi ? 1 : nin);
+  const int items = (g.nx / TXC) * outer * (multi ? 1 : nin);
   const int threads = NL * TXC * L::T;
   cudaFuncSetAttribute(k_pstrided<N, MODE, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_pstrided<N, MODE, C><<<grid, threads, sm, st>>>(g, axis, TXC, NIN, NOUT, Z, op);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pstrided<N, MODE, C>, threads, sm);
+  if (per_sm < 1) per_sm = 1;
+  int dev = 0, nsm = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int blocks = nsm * per_sm;
+  if (blocks > items) blocks = items;
+  k_pstrided<N, MODE, C><<<blocks, threads, sm, st>>>(g, axis, TXC, NIN, NOUT, Z, op, items);
   count_launch();
 }
 

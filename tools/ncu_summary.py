@@ -31,10 +31,12 @@ def main(path, top=8):
                 d[k] = r[hdr.index(k)]
                 print(f"   {k:70s} {r[hdr.index(k)]}")
         st = [(hdr[i], r[i]) for i in range(len(hdr))
-              if "warp_issue_stalled" in hdr[i] and hdr[i].endswith("per_warp_active.pct") and r[i]]
-        st = sorted(st, key=lambda x: -float(x[1]))[:top]
+              if hdr[i].startswith("smsp__average_warps_issue_stalled_") and hdr[i].endswith("_per_issue_active.ratio")
+              and r[i]]
+        st = sorted(st, key=lambda x: -float(x[1].replace(",", "")))[:top]
         for s in st:
-            print(f"      stall {s[0].replace('smsp__warp_issue_stalled_', ''):55s} {s[1]}")
+            nm = s[0].replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", "")
+            print(f"      stall {nm:40s} {s[1]}")
         res.append((name, d))
     return res
 
