@@ -219,7 +219,7 @@ topt_status topt_mix(topt_ctx* ctx, const float* q, const float* const* vs, cons
  * Synchronizes the device. */
 topt_status topt_profile(topt_ctx* ctx, int32_t enable);
 
-/* Accumulated stats of kernel class `cls` (0..10; TOPT_ERR_INVALID_ARG past the end): class
+/* Accumulated stats of kernel class `cls` (0..9; TOPT_ERR_INVALID_ARG past the end): class
  * name (static string), total event-timed ms, total ALGORITHMIC bytes (each operand read
  * once, each result written once per launch) and kernel launches.
  * Synchronizes on the recorded events. */

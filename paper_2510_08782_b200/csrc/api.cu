@@ -272,11 +272,12 @@ constexpr int kSet = 32;  // doubles per scalar set: [0, 16) public, [16, 32) in
 
 // Kernel classes for topt_kernel_stats; bytes are ALGORITHMIC (each operand read once,
 // each result written once per launch group).
-enum KClass { K_TRACE, K_SL_FWD, K_SL_LAST, K_SL_ADJ, K_EFACTOR, K_DIV, K_BODY, K_VCHAIN, K_BCHAIN, K_ASSEMBLE,
-              K_MISC, K_NCLASS };
-const char* kClassNames[K_NCLASS] = {"sl_trace",  "sl_step_fwd", "sl_step_last", "sl_step_adj",
-                                     "efactor",   "div_v",       "body_force",   "vchain_alphaLv",
-                                     "bchain_fft", "assemble",   "misc"};
+// K_SL_STEP: every interior SL step of both sweeps (one kernel, forward with/without E and
+// adjoint); the last forward step (fused mismatch) is its own class.
+enum KClass { K_TRACE, K_SL_STEP, K_SL_LAST, K_EFACTOR, K_DIV, K_BODY, K_VCHAIN, K_BCHAIN, K_ASSEMBLE, K_MISC,
+              K_NCLASS };
+const char* kClassNames[K_NCLASS] = {"sl_trace", "sl_step",        "sl_step_last", "efactor",  "div_v",
+                                     "body_force", "vchain_alphaLv", "bchain_fft",   "assemble", "misc"};
 
 cudaEvent_t take_event(topt_ctx* c) {
   if (!c->pool.empty()) {
@@ -366,7 +367,7 @@ void forward_half(topt_ctx* c, const float* m0, const float* m1, const float* v,
     cudaMemcpyAsync(c->m_traj, m0, F * 4, cudaMemcpyDeviceToDevice, st);
   }
   for (int j = 0; j + 1 < S; ++j) {
-    Prof pr(c, K_SL_FWD, (d + 2 + e) * F4, 1, st);
+    Prof pr(c, K_SL_STEP, (d + 2 + e) * F4, 1, st);
     launch_sl_step(g, c->m_traj + j * F, c->df, Ef, c->m_traj + (j + 1) * F, st);
   }
   {
@@ -400,7 +401,7 @@ void backward_half(topt_ctx* c, const float* v, const float* u, float* gout, flo
   }
   const double e = Ea ? 1.0 : 0.0;
   for (int j = S - 1; j >= 0; --j) {
-    Prof pr(c, K_SL_ADJ, (d + 2 + e) * F4, 1, st);
+    Prof pr(c, K_SL_STEP, (d + 2 + e) * F4, 1, st);
     launch_sl_step(g, c->lam_traj + (j + 1) * F, c->da, Ea, c->lam_traj + j * F, st);
   }
   std::vector<double> w = c->wts;
