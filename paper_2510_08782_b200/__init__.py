@@ -73,7 +73,14 @@ class Config:
 
 
 class Topt:
-    """One problem context bound to a CUDA device and a torch-allocated workspace."""
+    """One problem context bound to a CUDA device and a torch-allocated workspace.
+
+    world > 1 splits the grid into z-slabs.  With ``unique_id`` (from
+    ``get_unique_id`` on rank 0, broadcast with torch.distributed) each process owns one slab
+    and exchanges over NCCL; fields passed in and out are that rank's slab
+    [nz/world][ny][nx].  Without it, one process emulates all ``world`` slabs on one GPU
+    (exchanges become device copies) and fields are whole-grid arrays — used to test that the
+    decomposition reproduces the single-slab result."""
 
     def __init__(self, cfg: Config, device=None, rank: int = 0, world: int = 1, unique_id: bytes | None = None):
         if not torch.cuda.is_available():
@@ -89,6 +96,14 @@ class Topt:
             check(LIB.topt_create(ctypes.byref(self._p), rank, world, uid, self.device.index,
                                   ctypes.byref(ctx)), "topt_create")
         self.ctx = ctx
+        self.rank, self.world = rank, world
+        z0, nz = ctypes.c_int32(), ctypes.c_int32()
+        check(LIB.topt_local_slab(self.ctx, ctypes.byref(z0), ctypes.byref(nz)), "topt_local_slab")
+        if self.d == 3:  # NCCL z-slabs: this rank's planes [z0, z0 + nz); emulation: the whole grid
+            self.z0 = z0.value
+            self.shape = (nz.value,) + self.shape[1:]
+        else:
+            self.z0 = 0
         nbytes = ctypes.c_size_t()
         check(LIB.topt_workspace_size(self.ctx, ctypes.byref(nbytes)), "topt_workspace_size")
         self.workspace = torch.empty(nbytes.value + 256, dtype=torch.uint8, device=self.device)
@@ -230,6 +245,13 @@ class Topt:
         out = rep.as_dict()
         out["exit_name"] = EXIT.get(rep.exit, rep.exit)
         return v, out
+
+
+def get_unique_id() -> bytes:
+    """NCCL unique id for topt_create (rank 0; broadcast it to the other ranks)."""
+    buf = ctypes.create_string_buffer(128)
+    check(LIB.topt_get_unique_id(buf), "topt_get_unique_id")
+    return buf.raw
 
 
 def solve(m0, m1, alpha, nt, model="advection", window=5, mixing_period=None, sigma=1, tau=0,

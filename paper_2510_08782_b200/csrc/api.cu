@@ -1,5 +1,6 @@
 // api.cu — C ABI of libtopt: context, workspace, gradient evaluation and the GA-NGMRES
-// driver (host logic; every field operation runs in the kernels of kernels_*.cu).
+// driver (host logic; every field operation runs in the kernels of kernels_*.cu, every
+// exchange between z-slabs in dist.cu).
 //
 // PAPER.md anchors: objective (1.1a) P:25-29; reduced gradient (2.2) P:105-108;
 // adjoint (2.3) P:110-121 (R1); time grid/trapezoid P:126; kernel fix P:134; SL RK2
@@ -13,16 +14,22 @@
 #include <cstdio>
 #include <cstring>
 #include <deque>
+#include <functional>
 #include <string>
 #include <vector>
 
-#include "internal.cuh"
-
-#ifdef TOPT_WITH_NCCL
-#include <nccl.h>
-#endif
+#include "ctx.cuh"
 
 using namespace topt;
+
+namespace topt {
+bool comm_halo(topt_ctx* c, const std::vector<float*>& base, int nf, size_t fstride, cudaStream_t st);
+bool comm_z2y(topt_ctx* c, const std::vector<const char*>& src, const std::vector<char*>& dst, size_t eb,
+              cudaStream_t st);
+bool comm_y2z(topt_ctx* c, const std::vector<const char*>& src, const std::vector<char*>& dst, size_t eb,
+              cudaStream_t st);
+bool comm_allreduce(topt_ctx* c, const std::vector<double*>& ptr, int count, bool is_max, cudaStream_t st);
+}  // namespace topt
 
 namespace {
 
@@ -47,44 +54,6 @@ int ilog2(int n) { int l = 0; while ((1 << l) < n) ++l; return l; }
 size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 }  // namespace
-
-struct topt_ctx {
-  topt_params p{};
-  int rank = 0, world = 1, device = 0;
-  Geom g{};
-  int d = 3;
-  int nzg = 1;  // global n[2]
-  int z0 = 0;
-  size_t F = 0;     // local points per scalar field
-  size_t vecN = 0;  // d * F
-  double h[3]{}, dt = 0, cellvol = 0;
-  std::vector<double> wts;  // trapezoid weights (R10)
-  // workspace
-  char* ws = nullptr;
-  size_t ws_bytes = 0, ws_need = 0;
-  float *m_traj{}, *lam_traj{}, *df{}, *da{}, *E{}, *divv{}, *b{}, *utmp{};
-  float2* Z{};      // b-chain: 4 complex fields of F
-  double2* Zv{};    // v-chain: 3 double-complex fields of F
-  float *m0b{}, *m1b{}, *vb{}, *vt{};
-  float *vcur{}, *gcur{}, *scur{}, *q{}, *gq{}, *sq{}, *vnew{}, *gnew{}, *snew{};
-  float *ucur{}, *uq{}, *unew{};  // u = alpha L v tracked alongside v
-  float* hist{};  // (w+1) slots x 3 vectors (NGMRES: v, g, u; AA: r, q, u(q))
-  double* partials{};
-  double* sc{};    // 5 sets of 32: [0..15] public, [16..31] internal; sets: current, trial, q, new, scratch
-  double* dots{};  // kMaxVecs doubles
-  bool have_eval = false;
-  std::vector<double> replay;
-  // per-kernel-class timing (topt_profile / topt_kernel_stats)
-  bool prof = false;
-  struct Rec { int cls; cudaEvent_t a, b; double bytes; int launches; };
-  std::vector<Rec> recs;
-  std::vector<cudaEvent_t> pool;
-  double pms[16]{}, pbytes[16]{};
-  long long plaunch[16]{};
-#ifdef TOPT_WITH_NCCL
-  ncclComm_t comm = nullptr;
-#endif
-};
 
 extern "C" {
 
@@ -124,25 +93,29 @@ static topt_status validate(const topt_params* p, int world) {
     return fail(TOPT_ERR_INVALID_ARG, "ordering");
   if (p->max_iter < 0 || !(p->eps_rel >= 0) || !(p->armijo_c > 0) || p->max_backtracks < 0)
     return fail(TOPT_ERR_INVALID_ARG, "stopping / line-search parameters");
-  if (world < 1) return fail(TOPT_ERR_INVALID_ARG, "world must be >= 1");
+  if (world < 1 || world > 64 || !pow2(world))
+    return fail(TOPT_ERR_INVALID_ARG, "world must be a power of two <= 64");
   if (world > 1) {
     if (p->dim != 3) return fail(TOPT_ERR_INVALID_ARG, "dim == 2 runs on one rank");
-    if (p->n[2] % world) return fail(TOPT_ERR_INVALID_ARG, "n[2] % world != 0");
+    if (p->n[2] % world || p->n[1] % world) return fail(TOPT_ERR_INVALID_ARG, "n[1] and n[2] must divide by world");
+    if (p->n[2] / world < kSlabHalo) return fail(TOPT_ERR_INVALID_ARG, "n[2] / world must be >= 4 (halo)");
+    if (p->n[0] < 32 || p->n[1] % 8) return fail(TOPT_ERR_UNSUPPORTED, "z-slabs need n[0] >= 32 and n[1] % 8 == 0");
   }
   return TOPT_OK;
 }
 
-topt_status topt_create(const topt_params* p, int32_t rank, int32_t world, const uint8_t* id,
-                        int32_t device, topt_ctx** out) {
+topt_status topt_create(const topt_params* p, int32_t rank, int32_t world, const uint8_t* id, int32_t device,
+                        topt_ctx** out) {
   if (!out) return fail(TOPT_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
   topt_status s = validate(p, world);
   if (s != TOPT_OK) return s;
   if (rank < 0 || rank >= world) return fail(TOPT_ERR_INVALID_ARG, "rank out of range");
-  if (world > 1) {
-    (void)id;
-    return fail(TOPT_ERR_UNSUPPORTED, "z-slab decomposition (world > 1) not built in this version");
-  }
+  const bool emulate = world > 1 && id == nullptr;
+  if (emulate && rank != 0) return fail(TOPT_ERR_INVALID_ARG, "emulated z-slabs (id == NULL) run as rank 0");
+#ifndef TOPT_WITH_NCCL
+  if (world > 1 && !emulate) return fail(TOPT_ERR_UNSUPPORTED, "libtopt built without NCCL");
+#endif
   TOPT_CUDA(cudaSetDevice(device));
   auto* c = new topt_ctx();
   c->p = *p;
@@ -151,49 +124,84 @@ topt_status topt_create(const topt_params* p, int32_t rank, int32_t world, const
   c->device = device;
   c->d = p->dim;
   c->nzg = p->dim == 3 ? p->n[2] : 1;
-  const int nzl = c->nzg / world;
-  c->z0 = rank * nzl;
-  Geom& g = c->g;
-  g.d = p->dim;
-  g.nx = p->n[0];
-  g.ny = p->n[1];
-  g.nz = nzl;
-  g.lx = ilog2(g.nx);
-  g.ly = ilog2(g.ny);
-  g.lz = ilog2(g.nz);
-  g.F = (size_t)g.nx * g.ny * g.nz;
-  c->F = g.F;
-  c->vecN = (size_t)c->d * g.F;
+  c->comm.P = world;
+  c->comm.nloc = emulate ? world : 1;
+#ifdef TOPT_WITH_NCCL
+  if (world > 1 && !emulate) {
+    ncclUniqueId u;
+    std::memcpy(u.internal, id, 128);
+    if (ncclCommInitRank(&c->comm.nccl, world, u, rank) != ncclSuccess) {
+      delete c;
+      return fail(TOPT_ERR_NCCL, "ncclCommInitRank failed");
+    }
+  }
+#endif
   c->dt = 1.0 / p->nt;
   c->cellvol = 1.0;
   for (int a = 0; a < c->d; ++a) {
     c->h[a] = 2.0 * M_PI / p->n[a];
     c->cellvol *= c->h[a];
   }
-  g.cx = (float)(c->dt / c->h[0]);
-  g.cy = (float)(c->dt / c->h[1]);
-  g.cz = c->d == 3 ? (float)(c->dt / c->h[2]) : 0.f;
   c->wts.assign(p->nt + 1, c->dt);
   c->wts.front() = c->wts.back() = 0.5 * c->dt;
-  // workspace size
-  const size_t F = g.F, V = c->vecN, S1 = p->nt + 1, W1 = p->window + 1;
+  const int nzl = c->nzg / world;
+  c->slabs.resize(c->comm.nloc);
+  for (int si = 0; si < c->comm.nloc; ++si) {
+    Slab& sl = c->slabs[si];
+    sl.index = emulate ? si : rank;
+    Geom& g = sl.g;
+    g.d = p->dim;
+    g.nx = p->n[0];
+    g.ny = p->n[1];
+    g.nz = nzl;
+    g.lx = ilog2(g.nx);
+    g.ly = ilog2(g.ny);
+    g.lz = ilog2(g.nz);
+    g.F = (size_t)g.nx * g.ny * g.nz;
+    g.cx = (float)(c->dt / c->h[0]);
+    g.cy = (float)(c->dt / c->h[1]);
+    g.cz = c->d == 3 ? (float)(c->dt / c->h[2]) : 0.f;
+    g.zh = world > 1 ? kSlabHalo : 0;
+    g.ky0 = 0;
+    g.nyg = 0;
+    g.haloerr = nullptr;
+    sl.gy = g;  // y-slab layout of the z passes: [nz][ny/P][nx]
+    sl.gy.ny = g.ny / world;
+    sl.gy.ly = ilog2(sl.gy.ny);
+    sl.gy.nz = c->nzg;
+    sl.gy.lz = ilog2(c->nzg);
+    sl.gy.zh = 0;
+    sl.gy.ky0 = sl.index * sl.gy.ny;
+    sl.gy.nyg = g.ny;
+    sl.F = g.F;
+    sl.plane = (size_t)g.nx * g.ny;
+    sl.Fh = g.F + 2 * (size_t)g.zh * sl.plane;
+  }
+  c->F = c->slabs[0].F;
+  c->vecN = (size_t)c->d * c->F;
+  // workspace size per slab
+  const Slab& s0 = c->slabs[0];
+  const size_t F = s0.F, Fh = s0.Fh, V = c->vecN, S1 = p->nt + 1, W1 = p->window + 1;
   size_t b = 0;
   auto add = [&](size_t bytes) { b += align256(bytes); };
-  add(S1 * F * 4);        // m_traj
-  add(S1 * F * 4);        // lam_traj
-  add(V * 4); add(V * 4); // df, da
-  add(F * 4); add(F * 4); // E, divv
-  add(V * 4);             // b
-  add(V * 4);             // utmp
-  add(4 * F * 8);         // Z (4 complex fields)
-  add(3 * F * 16);        // Zv (3 double-complex fields)
-  add(F * 4); add(F * 4); add(V * 4); add(V * 4);  // m0b, m1b, vb, vt
-  for (int i = 0; i < 12; ++i) add(V * 4);         // vcur..snew, ucur, uq, unew
-  add(3 * W1 * V * 4);    // history
+  add(S1 * Fh * 4); add(S1 * Fh * 4);                          // m_traj, lam_traj
+  add(world > 1 ? c->d * Fh * 4 : 0); add(Fh * 4);             // vh, divv
+  add(V * 4); add(V * 4); add(F * 4); add(V * 4); add(V * 4);  // df, da, E, b, utmp
+  add(4 * F * 8); add(3 * F * 16);                             // Z, Zv
+  if (world > 1) {
+    add(4 * F * 8); add(3 * F * 16);                           // Zy, Zvy
+    add(2 * S1 * F * 4); add(2 * F * 4);                       // ytraj, ytmp
+    add(16 * F);                                               // sendbuf
+  }
+  add(F * 4); add(F * 4); add(V * 4); add(V * 4);              // m0b, m1b, vb, vt
+  for (int i = 0; i < 12; ++i) add(V * 4);                     // solver vectors
+  add(3 * W1 * V * 4);                                         // history
   add((size_t)kNumSlots * kMaxPartials * 8);
-  add(5 * 32 * 8);
+  add(5 * kSet * 8);
   add(kMaxVecs * kMaxVecs * 8);
-  c->ws_need = b;
+  add(256);                                                    // halo error flag
+  c->slab_bytes = b;
+  c->ws_need = b * c->comm.nloc;
   upload_twiddles();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -209,7 +217,7 @@ topt_status topt_destroy(topt_ctx* ctx) {
   for (auto& r : ctx->recs) { ctx->pool.push_back(r.a); ctx->pool.push_back(r.b); }
   for (auto e : ctx->pool) cudaEventDestroy(e);
 #ifdef TOPT_WITH_NCCL
-  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->comm.nccl) ncclCommDestroy(ctx->comm.nccl);
 #endif
   delete ctx;
   return TOPT_OK;
@@ -227,57 +235,72 @@ topt_status topt_bind_workspace(topt_ctx* c, void* dptr, size_t bytes) {
   if (bytes < c->ws_need) return fail(TOPT_ERR_WORKSPACE, "workspace too small");
   c->ws = (char*)dptr;
   c->ws_bytes = bytes;
-  const size_t F = c->F, V = c->vecN, S1 = c->p.nt + 1, W1 = c->p.window + 1;
-  char* q = c->ws;
-  auto take = [&](size_t bytes_) { char* r = q; q += align256(bytes_); return r; };
-  c->m_traj = (float*)take(S1 * F * 4);
-  c->lam_traj = (float*)take(S1 * F * 4);
-  c->df = (float*)take(V * 4);
-  c->da = (float*)take(V * 4);
-  c->E = (float*)take(F * 4);
-  c->divv = (float*)take(F * 4);
-  c->b = (float*)take(V * 4);
-  c->utmp = (float*)take(V * 4);
-  c->Z = (float2*)take(4 * F * 8);
-  c->Zv = (double2*)take(3 * F * 16);
-  c->m0b = (float*)take(F * 4);
-  c->m1b = (float*)take(F * 4);
-  c->vb = (float*)take(V * 4);
-  c->vt = (float*)take(V * 4);
-  float** vecs[12] = {&c->vcur, &c->gcur, &c->scur, &c->q,    &c->gq,   &c->sq,
-                      &c->vnew, &c->gnew, &c->snew, &c->ucur, &c->uq,   &c->unew};
-  for (auto pp : vecs) *pp = (float*)take(V * 4);
-  c->hist = (float*)take(3 * W1 * V * 4);
-  c->partials = (double*)take((size_t)kNumSlots * kMaxPartials * 8);
-  c->sc = (double*)take(5 * 32 * 8);
-  c->dots = (double*)take(kMaxVecs * kMaxVecs * 8);
+  const int world = c->world;
+  for (int si = 0; si < c->comm.nloc; ++si) {
+    Slab& sl = c->slabs[si];
+    const size_t F = sl.F, Fh = sl.Fh, V = c->vecN, S1 = c->p.nt + 1, W1 = c->p.window + 1;
+    char* q = c->ws + si * c->slab_bytes;
+    auto take = [&](size_t bytes_) { char* r = q; q += align256(bytes_); return r; };
+    sl.m_traj = (float*)take(S1 * Fh * 4);
+    sl.lam_traj = (float*)take(S1 * Fh * 4);
+    sl.vh = (float*)take(world > 1 ? c->d * Fh * 4 : 0);
+    sl.divv = (float*)take(Fh * 4);
+    sl.df = (float*)take(V * 4);
+    sl.da = (float*)take(V * 4);
+    sl.E = (float*)take(F * 4);
+    sl.b = (float*)take(V * 4);
+    sl.utmp = (float*)take(V * 4);
+    sl.Z = (float2*)take(4 * F * 8);
+    sl.Zv = (double2*)take(3 * F * 16);
+    if (world > 1) {
+      sl.Zy = (float2*)take(4 * F * 8);
+      sl.Zvy = (double2*)take(3 * F * 16);
+      sl.ytraj = (float*)take(2 * S1 * F * 4);
+      sl.ytmp = (float*)take(2 * F * 4);
+      sl.sendbuf = take(16 * F);
+    }
+    sl.m0b = (float*)take(F * 4);
+    sl.m1b = (float*)take(F * 4);
+    sl.vb = (float*)take(V * 4);
+    sl.vt = (float*)take(V * 4);
+    float** vecs[12] = {&sl.vcur, &sl.gcur, &sl.scur, &sl.q,    &sl.gq,   &sl.sq,
+                        &sl.vnew, &sl.gnew, &sl.snew, &sl.ucur, &sl.uq,   &sl.unew};
+    for (auto pp : vecs) *pp = (float*)take(V * 4);
+    sl.hist = (float*)take(3 * W1 * V * 4);
+    sl.partials = (double*)take((size_t)kNumSlots * kMaxPartials * 8);
+    sl.sc = (double*)take(5 * kSet * 8);
+    sl.dots = (double*)take(kMaxVecs * kMaxVecs * 8);
+    sl.haloerr = (int*)take(256);
+    sl.g.haloerr = sl.haloerr;
+    sl.gy.haloerr = sl.haloerr;
+  }
+  for (auto& sl : c->slabs) TOPT_CUDA(cudaMemset(sl.haloerr, 0, sizeof(int)));
   return TOPT_OK;
 }
 
 topt_status topt_local_slab(const topt_ctx* ctx, int32_t* z0, int32_t* nz) {
   if (!ctx || !z0 || !nz) return fail(TOPT_ERR_INVALID_ARG, "NULL argument");
-  *z0 = ctx->z0;
-  *nz = ctx->d == 3 ? ctx->g.nz : 1;
+  const bool emu = ctx->comm.P > 1 && ctx->comm.emulated();
+  *z0 = emu ? 0 : ctx->slabs[0].index * ctx->slabs[0].g.nz;
+  *nz = ctx->d == 3 ? (emu ? ctx->nzg : ctx->slabs[0].g.nz) : 1;
   return TOPT_OK;
 }
 
 }  // extern "C"
 
 // ======================================================================================
-// Internal orchestration
+// Internal orchestration (loops over the local slabs; exchanges through dist.cu)
 // ======================================================================================
 namespace {
 
-constexpr int kSet = 32;  // doubles per scalar set: [0, 16) public, [16, 32) internal
-
 // Kernel classes for topt_kernel_stats; bytes are ALGORITHMIC (each operand read once,
-// each result written once per launch group).
-// K_SL_STEP: every interior SL step of both sweeps (one kernel, forward with/without E and
-// adjoint); the last forward step (fused mismatch) is its own class.
-enum KClass { K_TRACE, K_SL_STEP, K_SL_LAST, K_EFACTOR, K_DIV, K_BODY, K_VCHAIN, K_BCHAIN, K_ASSEMBLE, K_MISC,
-              K_NCLASS };
-const char* kClassNames[K_NCLASS] = {"sl_trace", "sl_step",        "sl_step_last", "efactor",  "div_v",
-                                     "body_force", "vchain_alphaLv", "bchain_fft",   "assemble", "misc"};
+// each result written once per launch group).  K_SL_STEP: every interior SL
+// step of both sweeps (one kernel); the last forward step (fused mismatch) is its own class.
+enum KClass { K_TRACE, K_SL_STEP, K_SL_LAST, K_EFACTOR, K_DIV, K_BODY, K_VCHAIN, K_BCHAIN, K_ASSEMBLE, K_COMM,
+              K_MISC, K_NCLASS };
+const char* kClassNames[K_NCLASS] = {"sl_trace",   "sl_step",        "sl_step_last", "efactor",  "div_v",
+                                     "body_force", "vchain_alphaLv", "bchain_fft",   "assemble", "comm",
+                                     "misc"};
 
 cudaEvent_t take_event(topt_ctx* c) {
   if (!c->pool.empty()) {
@@ -321,139 +344,312 @@ topt_status need_ws(topt_ctx* c) {
 }
 
 bool aligned16(const void* p) { return (((uintptr_t)p) & 15) == 0; }
+int P_of(const topt_ctx* c) { return c->comm.P; }
+double ntot(const topt_ctx* c) { return (double)c->F * c->comm.P; }
+float* local(const Slab& s, float* base) { return base + (size_t)s.g.zh * s.plane; }
 
-double* pub(topt_ctx* c, int set) { return c->sc + set * kSet; }
-double* intl(topt_ctx* c, int set) { return c->sc + set * kSet + 16; }
+// Per-slab inputs / outputs of one evaluation.
+struct Io {
+  const float* m0;
+  const float* m1;
+  const float* v;   // d*F local layout
+  const float* u;   // alpha L v (d*F) or null
+  float* g;
+  float* s;
+  double* scal;     // public scalars
+  double* isc;      // internal scalars
+};
 
-// div v = sum_a d_a v_a (R3), into c->divv
-void compute_div(topt_ctx* c, const float* v, cudaStream_t st) {
+std::vector<double*> pubs(std::vector<Io>& io, int off) {
+  std::vector<double*> r;
+  for (auto& x : io) r.push_back(x.scal + off);
+  return r;
+}
+std::vector<double*> intls(std::vector<Io>& io, int off) {
+  std::vector<double*> r;
+  for (auto& x : io) r.push_back(x.isc + off);
+  return r;
+}
+
+// z-slab <-> y-slab transposes of one field per slab
+template <typename T>
+bool tz2y(topt_ctx* c, const std::vector<T*>& src, const std::vector<T*>& dst, cudaStream_t st) {
+  std::vector<const char*> s;
+  std::vector<char*> d;
+  for (auto p : src) s.push_back((const char*)p);
+  for (auto p : dst) d.push_back((char*)p);
+  Prof pr(c, K_COMM, 2.0 * sizeof(T) * c->F * c->comm.nloc, 0, st);
+  return comm_z2y(c, s, d, sizeof(T), st);
+}
+template <typename T>
+bool ty2z(topt_ctx* c, const std::vector<T*>& src, const std::vector<T*>& dst, cudaStream_t st) {
+  std::vector<const char*> s;
+  std::vector<char*> d;
+  for (auto p : src) s.push_back((const char*)p);
+  for (auto p : dst) d.push_back((char*)p);
+  Prof pr(c, K_COMM, 2.0 * sizeof(T) * c->F * c->comm.nloc, 0, st);
+  return comm_y2z(c, s, d, sizeof(T), st);
+}
+bool halo(topt_ctx* c, std::function<float*(Slab&)> base, int nf, size_t fstride, cudaStream_t st) {
+  if (P_of(c) == 1) return true;
+  std::vector<float*> b;
+  for (auto& sl : c->slabs) b.push_back(base(sl));
+  const Slab& s0 = c->slabs[0];
+  Prof pr(c, K_COMM, 4.0 * nf * s0.g.zh * s0.plane * 4.0 * c->comm.nloc, 0, st);
+  return comm_halo(c, b, nf, fstride, st);
+}
+
+// div v = sum_a d_a v_a (R3), into the local planes of divv; halo refreshed
+void compute_div(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
+  const int P = P_of(c);
   double one = 1.0;
-  for (int a = 0; a < c->d; ++a) {
-    DerivArgs da{v + a * c->F, 0, nullptr, 0, &one, 1, a == 0 ? 0.f : 1.f, c->divv};
-    launch_deriv_accum(c->g, a, da, st);
+  for (size_t si = 0; si < c->slabs.size(); ++si) {
+    Slab& sl = c->slabs[si];
+    const int na = P > 1 ? 2 : c->d;  // z handled by the transpose below when P > 1
+    for (int a = 0; a < na; ++a) {
+      DerivArgs da{io[si].v + a * sl.F, 0, nullptr, 0, &one, 1, a == 0 ? 0.f : 1.f, local(sl, sl.divv)};
+      launch_deriv_accum(sl.g, a, da, st);
+    }
+  }
+  if (P > 1) {
+    std::vector<float*> src, dst, ysrc, back;
+    for (size_t si = 0; si < c->slabs.size(); ++si) {
+      src.push_back(const_cast<float*>(io[si].v) + 2 * c->slabs[si].F);
+      dst.push_back(c->slabs[si].ytmp);
+    }
+    tz2y(c, src, dst, st);
+    for (auto& sl : c->slabs) {
+      DerivArgs da{sl.ytmp, 0, nullptr, 0, &one, 1, 0.f, sl.ytmp + sl.F};
+      launch_deriv_accum(sl.gy, 2, da, st);
+      ysrc.push_back(sl.ytmp + sl.F);
+      back.push_back(sl.utmp);
+    }
+    ty2z(c, ysrc, back, st);
+    for (auto& sl : c->slabs) launch_axpy(local(sl, sl.divv), 1.0f, sl.utmp, sl.F, local(sl, sl.divv), st);
+    halo(c, [](Slab& s) { return s.divv; }, 1, 0, st);
   }
 }
 
-// Forward half: feet (R6), static factor (continuity, R7), m^0..m^S in m_traj,
-// lam^S = m1 - m^S (R1/R8), dist -> scal[DIST], sum_x v_c -> isc[I_SUMV..].
-void forward_half(topt_ctx* c, const float* m0, const float* m1, const float* v, bool want_adj, double* scal,
-                  double* isc, cudaStream_t st) {
-  const Geom& g = c->g;
-  const int S = c->p.nt;
-  const size_t F = c->F;
-  const double F4 = 4.0 * F, d = c->d;
-  int np = 0;
-  {
-    Prof pr(c, K_TRACE, (d + d * (want_adj ? 2 : 1)) * F4, 1, st);
-    launch_trace(g, v, c->df, want_adj ? c->da : nullptr, c->partials, &np, st);
+// Forward half: feet (R6), static factor (continuity, R7), m^0..m^S, lam^S = m1 - m^S
+// (R1/R8), dist -> scal[DIST], sum_x v_c -> isc[I_SUMV..] (all-reduced).
+void forward_half(topt_ctx* c, std::vector<Io>& io, bool want_adj, cudaStream_t st) {
+  const int S = c->p.nt, P = P_of(c);
+  const double F4 = 4.0 * c->F, d = c->d;
+  if (P > 1) {  // halo'd copy of v for the trace
+    for (size_t si = 0; si < c->slabs.size(); ++si) {
+      Slab& sl = c->slabs[si];
+      for (int a = 0; a < c->d; ++a)
+        cudaMemcpyAsync(local(sl, sl.vh + a * sl.Fh), io[si].v + a * sl.F, sl.F * 4, cudaMemcpyDeviceToDevice, st);
+    }
+    halo(c, [](Slab& s) { return s.vh; }, c->d, c->slabs[0].Fh, st);
   }
-  {
+  for (size_t si = 0; si < c->slabs.size(); ++si) {
+    Slab& sl = c->slabs[si];
+    int np = 0;
+    {
+      Prof pr(c, K_TRACE, (d + d * (want_adj ? 2 : 1)) * F4, 1, st);
+      launch_trace(sl.g, P > 1 ? sl.vh : io[si].v, sl.df, want_adj ? sl.da : nullptr, sl.partials, &np, st);
+    }
     Prof pr(c, K_MISC, 0.0, 1, st);
-    launch_finalize_slots(c->partials, 0, c->d, np, false, isc + I_SUMV, st);
+    launch_finalize_slots(sl.partials, 0, c->d, np, false, io[si].isc + I_SUMV, st);
   }
-  const float* Ef = nullptr;
-  if (c->p.model == TOPT_CONTINUITY) {
+  comm_allreduce(c, intls(io, I_SUMV), c->d, false, st);
+  const bool cont = c->p.model == TOPT_CONTINUITY;
+  if (cont) {
     {
       Prof pr(c, K_DIV, (3.0 * d - 1.0) * F4, c->d, st);
-      compute_div(c, v, st);
+      compute_div(c, io, st);
     }
-    Prof pr(c, K_EFACTOR, (d + 2) * F4, 1, st);
-    launch_efactor(g, c->divv, c->df, (float)(-0.5 * c->dt), (float)(0.5 * c->dt * c->dt), c->E, st);
-    Ef = c->E;
+    for (auto& sl : c->slabs) {
+      Prof pr(c, K_EFACTOR, (d + 2) * F4, 1, st);
+      launch_efactor(sl.g, sl.divv, sl.df, (float)(-0.5 * c->dt), (float)(0.5 * c->dt * c->dt), sl.E, st);
+    }
   }
-  const double e = Ef ? 1.0 : 0.0;
-  {
+  const double e = cont ? 1.0 : 0.0;
+  for (size_t si = 0; si < c->slabs.size(); ++si) {
+    Slab& sl = c->slabs[si];
     Prof pr(c, K_MISC, 2.0 * F4, 0, st);
-    cudaMemcpyAsync(c->m_traj, m0, F * 4, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(local(sl, sl.m_traj), io[si].m0, sl.F * 4, cudaMemcpyDeviceToDevice, st);
   }
-  for (int j = 0; j + 1 < S; ++j) {
-    Prof pr(c, K_SL_STEP, (d + 2 + e) * F4, 1, st);
-    launch_sl_step(g, c->m_traj + j * F, c->df, Ef, c->m_traj + (j + 1) * F, st);
+  std::vector<int> np(c->slabs.size(), 0);
+  for (int j = 0; j < S; ++j) {
+    halo(c, [j](Slab& s) { return s.m_traj + j * s.Fh; }, 1, 0, st);
+    for (size_t si = 0; si < c->slabs.size(); ++si) {
+      Slab& sl = c->slabs[si];
+      const float* Ef = cont ? sl.E : nullptr;
+      if (j + 1 < S) {
+        Prof pr(c, K_SL_STEP, (d + 2 + e) * F4, 1, st);
+        launch_sl_step(sl.g, sl.m_traj + j * sl.Fh, sl.df, Ef, local(sl, sl.m_traj + (j + 1) * sl.Fh), st);
+      } else {
+        Prof pr(c, K_SL_LAST, (d + 4 + e) * F4, 1, st);
+        launch_sl_last(sl.g, sl.m_traj + j * sl.Fh, sl.df, Ef, io[si].m1, local(sl, sl.m_traj + S * sl.Fh),
+                       local(sl, sl.lam_traj + S * sl.Fh), sl.partials, &np[si], st);
+      }
+    }
   }
-  {
-    Prof pr(c, K_SL_LAST, (d + 4 + e) * F4, 1, st);
-    launch_sl_last(g, c->m_traj + (S - 1) * F, c->df, Ef, m1, c->m_traj + S * F, c->lam_traj + S * F, c->partials,
-                   &np, st);
+  for (size_t si = 0; si < c->slabs.size(); ++si) {
+    Prof pr(c, K_MISC, 0.0, 1, st);
+    launch_finalize(c->slabs[si].partials, 0, np[si], 0.5 * c->cellvol, false, io[si].scal + TOPT_S_DIST, st);
   }
-  Prof pr(c, K_MISC, 0.0, 1, st);
-  launch_finalize(c->partials, 0, np, 0.5 * c->cellvol, false, scal + TOPT_S_DIST, st);
+  comm_allreduce(c, pubs(io, TOPT_S_DIST), 1, false, st);
 }
 
 // Backward half: adjoint sweep (advection: Heun factor, R7), body force (2.2)/(R8) with
 // trapezoid weights (R10), then g = alpha L v + b (P_L b for incompressible, R9) and
 // s = -(alpha L~)^{-1} g = -P_0 v - (alpha L~)^{-1} b.  alpha L v is `u` when the
-// caller tracks it (solver), otherwise computed by the fp64 v-chain.
-void backward_half(topt_ctx* c, const float* v, const float* u, float* gout, float* sout, double* scal,
-                   double* isc, cudaStream_t st) {
-  const Geom& g = c->g;
-  const int S = c->p.nt;
+// caller tracks it (solver), otherwise computed by the fp64 v-chain into utmp.
+void backward_half(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
+  const int S = c->p.nt, P = P_of(c);
   const size_t F = c->F;
   const double F4 = 4.0 * F, d = c->d;
-  const float* Ea = nullptr;
-  if (c->p.model == TOPT_ADVECTION) {
+  const bool adv = c->p.model == TOPT_ADVECTION;
+  if (adv) {
     {
       Prof pr(c, K_DIV, (3.0 * d - 1.0) * F4, c->d, st);
-      compute_div(c, v, st);
+      compute_div(c, io, st);
     }
-    Prof pr(c, K_EFACTOR, (d + 2) * F4, 1, st);
-    launch_efactor(g, c->divv, c->da, (float)(0.5 * c->dt), (float)(0.5 * c->dt * c->dt), c->E, st);
-    Ea = c->E;
+    for (auto& sl : c->slabs) {
+      Prof pr(c, K_EFACTOR, (d + 2) * F4, 1, st);
+      launch_efactor(sl.g, sl.divv, sl.da, (float)(0.5 * c->dt), (float)(0.5 * c->dt * c->dt), sl.E, st);
+    }
   }
-  const double e = Ea ? 1.0 : 0.0;
+  const double e = adv ? 1.0 : 0.0;
   for (int j = S - 1; j >= 0; --j) {
-    Prof pr(c, K_SL_STEP, (d + 2 + e) * F4, 1, st);
-    launch_sl_step(g, c->lam_traj + (j + 1) * F, c->da, Ea, c->lam_traj + j * F, st);
+    halo(c, [j](Slab& s) { return s.lam_traj + (j + 1) * s.Fh; }, 1, 0, st);
+    for (auto& sl : c->slabs) {
+      Prof pr(c, K_SL_STEP, (d + 2 + e) * F4, 1, st);
+      launch_sl_step(sl.g, sl.lam_traj + (j + 1) * sl.Fh, sl.da, adv ? sl.E : nullptr,
+                     local(sl, sl.lam_traj + j * sl.Fh), st);
+    }
   }
+  // body force
   std::vector<double> w = c->wts;
   const bool cont = c->p.model == TOPT_CONTINUITY;
   if (cont)
     for (auto& x : w) x = -x;
-  for (int a = 0; a < c->d; ++a) {
-    Prof pr(c, K_BODY, (2.0 * (S + 1) + 1.0) * F4, 1, st);
-    DerivArgs da{cont ? c->lam_traj : c->m_traj, F, cont ? c->m_traj : c->lam_traj, F, w.data(), S + 1, 0.f,
-                 c->b + a * F};
-    launch_deriv_accum(g, a, da, st);
+  const int nloc_axes = P > 1 ? 2 : c->d;
+  for (auto& sl : c->slabs) {
+    float* psi = local(sl, cont ? sl.lam_traj : sl.m_traj);
+    float* lam = local(sl, cont ? sl.m_traj : sl.lam_traj);
+    for (int a = 0; a < nloc_axes; ++a) {
+      Prof pr(c, K_BODY, (2.0 * (S + 1) + 1.0) * F4, 1, st);
+      DerivArgs da{psi, sl.Fh, lam, sl.Fh, w.data(), S + 1, 0.f, sl.b + a * F};
+      launch_deriv_accum(sl.g, a, da, st);
+    }
+  }
+  if (P > 1) {  // z axis in the y-slab layout: transpose all S+1 slices of psi and lam
+    for (int j = 0; j <= S; ++j)
+      for (int which = 0; which < 2; ++which) {  // 0: psi, 1: lam
+        std::vector<float*> src, dst;
+        for (auto& sl : c->slabs) {
+          float* traj = ((which == 0) == cont) ? sl.lam_traj : sl.m_traj;
+          src.push_back(local(sl, traj + j * sl.Fh));
+          dst.push_back(sl.ytraj + ((size_t)which * (S + 1) + j) * F);
+        }
+        tz2y(c, src, dst, st);
+      }
+    std::vector<float*> ysrc, zdst;
+    for (auto& sl : c->slabs) {
+      Prof pr(c, K_BODY, (2.0 * (S + 1) + 1.0) * F4, 1, st);
+      DerivArgs da{sl.ytraj, F, sl.ytraj + (S + 1) * F, F, w.data(), S + 1, 0.f, sl.ytmp};
+      launch_deriv_accum(sl.gy, 2, da, st);
+      ysrc.push_back(sl.ytmp);
+      zdst.push_back(sl.b + 2 * F);
+    }
+    ty2z(c, ysrc, zdst, st);
   }
   const bool leray = c->p.model == TOPT_INCOMPRESSIBLE;
   const double half = c->d == 3 ? 2.0 : 1.0;
-  if (!u) {
+  const double n_all = ntot(c);
+  // v-chain: u = alpha L v (fp64) when not supplied
+  const bool need_u = io[0].u == nullptr;
+  if (need_u) {
     const double nin = leray ? d : half, nout = half, F16 = 16.0 * F;
     const double bytes = d * F4 + nin * F16 + (c->d == 3 ? 2 * nin * F16 + 2 * nout * F16 : 0.0) +
                          (nin + nout) * F16 + nout * F16 + d * F4;
-    Prof pr(c, K_VCHAIN, bytes, c->d == 3 ? 5 : 3, st);
-    launch_vchain(g, v, c->Zv, c->utmp, c->p.alpha, c->p.reg_order, leray, st);
-    u = c->utmp;
+    Prof pr(c, K_VCHAIN, bytes * c->comm.nloc, c->d == 3 ? 5 : 3, st);
+    const int vin = vchain_nin(c->slabs[0].g, leray), vout = vchain_nout(c->slabs[0].g);
+    for (size_t si = 0; si < c->slabs.size(); ++si) {
+      Slab& sl = c->slabs[si];
+      double2* Z[3] = {sl.Zv, sl.Zv + F, sl.Zv + 2 * F};
+      vchain_xy(sl.g, io[si].v, Z, leray, st);
+    }
+    if (P > 1)
+      for (int f = 0; f < vin; ++f) {
+        std::vector<double2*> a, b;
+        for (auto& sl : c->slabs) { a.push_back(sl.Zv + f * F); b.push_back(sl.Zvy + f * F); }
+        tz2y(c, a, b, st);
+      }
+    for (auto& sl : c->slabs) {
+      double2* base = P > 1 ? sl.Zvy : sl.Zv;
+      double2* Z[3] = {base, base + F, base + 2 * F};
+      vchain_last(P > 1 ? sl.gy : sl.g, Z, c->p.alpha, c->p.reg_order, leray, n_all, st);
+    }
+    if (P > 1)
+      for (int f = 0; f < vout; ++f) {
+        std::vector<double2*> a, b;
+        for (auto& sl : c->slabs) { a.push_back(sl.Zvy + f * F); b.push_back(sl.Zv + f * F); }
+        ty2z(c, a, b, st);
+      }
+    for (size_t si = 0; si < c->slabs.size(); ++si) {
+      Slab& sl = c->slabs[si];
+      double2* Z[3] = {sl.Zv, sl.Zv + F, sl.Zv + 2 * F};
+      vchain_inv(sl.g, Z, sl.utmp, st);
+      io[si].u = sl.utmp;
+    }
   }
   {
     const double nin = leray ? d : half, nout = leray ? 2 * half : half, F8 = 8.0 * F;
     const double bytes = d * F4 + nin * F8 + (c->d == 3 ? 2 * nin * F8 + 2 * nout * F8 : 0.0) + (nin + nout) * F8;
-    Prof pr(c, K_BCHAIN, bytes, c->d == 3 ? 4 : 2, st);
-    launch_bchain(g, c->b, c->Z, c->p.alpha, c->p.reg_order, leray, st);
+    Prof pr(c, K_BCHAIN, bytes * c->comm.nloc, c->d == 3 ? 4 : 2, st);
+    const int bin = bchain_nin(c->slabs[0].g, leray), bout = bchain_nout(c->slabs[0].g, leray);
+    for (auto& sl : c->slabs) {
+      float2* Z[4] = {sl.Z, sl.Z + F, sl.Z + 2 * F, sl.Z + 3 * F};
+      bchain_xy(sl.g, sl.b, Z, leray, st);
+    }
+    if (P > 1)
+      for (int f = 0; f < bin; ++f) {
+        std::vector<float2*> a, b;
+        for (auto& sl : c->slabs) { a.push_back(sl.Z + f * F); b.push_back(sl.Zy + f * F); }
+        tz2y(c, a, b, st);
+      }
+    for (auto& sl : c->slabs) {
+      float2* base = P > 1 ? sl.Zy : sl.Z;
+      float2* Z[4] = {base, base + F, base + 2 * F, base + 3 * F};
+      bchain_last(P > 1 ? sl.gy : sl.g, Z, c->p.alpha, c->p.reg_order, leray, n_all, st);
+    }
+    if (P > 1)
+      for (int f = 0; f < bout; ++f) {
+        std::vector<float2*> a, b;
+        for (auto& sl : c->slabs) { a.push_back(sl.Zy + f * F); b.push_back(sl.Z + f * F); }
+        ty2z(c, a, b, st);
+      }
+    for (auto& sl : c->slabs) {
+      float2* Z[4] = {sl.Z, sl.Z + F, sl.Z + 2 * F, sl.Z + 3 * F};
+      bchain_yinv(sl.g, Z, leray, st);
+    }
   }
-  int np = 0;
-  {
-    const double nout = leray ? 2 * half : half;
-    const double bytes = nout * 8.0 * F + (leray ? 0.0 : d * F4) + 2 * d * F4 + 2 * d * F4;
-    Prof pr(c, K_ASSEMBLE, bytes, 1, st);
-    launch_assemble(g, c->Z, leray, c->b, u, v, isc + I_SUMV, gout, sout, c->partials, &np, st);
+  for (size_t si = 0; si < c->slabs.size(); ++si) {
+    Slab& sl = c->slabs[si];
+    int np = 0;
+    {
+      const double nout = leray ? 2 * half : half;
+      const double bytes = nout * 8.0 * F + (leray ? 0.0 : d * F4) + 2 * d * F4 + 2 * d * F4;
+      Prof pr(c, K_ASSEMBLE, bytes, 1, st);
+      launch_assemble(sl.g, sl.Z, leray, sl.b, io[si].u, io[si].v, io[si].isc + I_SUMV, io[si].g, io[si].s,
+                      sl.partials, &np, st, n_all);
+    }
+    Prof pr(c, K_MISC, 0.0, 1, st);
+    launch_finalize_slots(sl.partials, 0, 10, np, true, io[si].isc + I_GMAX, st);
   }
-  Prof pr(c, K_MISC, 0.0, 2, st);
-  launch_finalize_slots(c->partials, 0, 10, np, true, isc + I_GMAX, st);
-  launch_finish(isc, scal, c->d, (double)F, c->cellvol, st);
+  comm_allreduce(c, intls(io, I_GMAX), 1, true, st);
+  comm_allreduce(c, intls(io, I_GS), I_SUMS + 3 - I_GS, false, st);
+  for (size_t si = 0; si < c->slabs.size(); ++si) launch_finish(io[si].isc, io[si].scal, c->d, n_all, c->cellvol, st);
 }
 
-topt_status eval_gradient(topt_ctx* c, const float* m0, const float* m1, const float* v, const float* u,
-                          float* gout, float* sout, double* scal, double* isc, cudaStream_t st) {
-  forward_half(c, m0, m1, v, true, scal, isc, st);
-  backward_half(c, v, u, gout, sout, scal, isc, st);
-  TOPT_CHECK_LAUNCH();
-  return TOPT_OK;
-}
-
-// Forward-only trial objective (the Armijo trial): scal[DIST].
-topt_status trial_dist(topt_ctx* c, const float* m0, const float* m1, const float* v, double* scal, double* isc,
-                       cudaStream_t st) {
-  forward_half(c, m0, m1, v, false, scal, isc, st);
+topt_status eval_gradient(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
+  forward_half(c, io, true, st);
+  backward_half(c, io, st);
   TOPT_CHECK_LAUNCH();
   return TOPT_OK;
 }
@@ -526,34 +722,110 @@ struct HostScalars {
 };
 
 topt_status fetch(topt_ctx* c, int set, HostScalars& out, cudaStream_t st) {
-  TOPT_CUDA(cudaMemcpyAsync(out.v, c->sc + set * kSet, sizeof(out.v), cudaMemcpyDeviceToHost, st));
+  TOPT_CUDA(cudaMemcpyAsync(out.v, c->slabs[0].sc + set * kSet, sizeof(out.v), cudaMemcpyDeviceToHost, st));
+  std::vector<int> h(c->slabs.size(), 0);
+  for (size_t si = 0; si < c->slabs.size(); ++si)
+    TOPT_CUDA(cudaMemcpyAsync(&h[si], c->slabs[si].haloerr, sizeof(int), cudaMemcpyDeviceToHost, st));
   TOPT_CUDA(cudaStreamSynchronize(st));
+  for (int x : h)
+    if (x) return fail(TOPT_ERR_HALO, "a characteristic foot left the z-slab halo (|delta_z| > 3 cells)");
   return TOPT_OK;
 }
 
-// dots[i] = <a, bs[i]> (unweighted l2 over d*F entries), returned on the host
-topt_status host_dots(topt_ctx* c, const float* a, const std::vector<const float*>& bs, std::vector<double>& out,
+// dots[i] = <a, bs[i]> (unweighted l2 over all d*n entries of all slabs), on the host.
+topt_status host_dots(topt_ctx* c, std::function<const float*(Slab&)> a,
+                      const std::vector<std::function<const float*(Slab&)>>& bs, std::vector<double>& out,
                       cudaStream_t st) {
-  out.assign(bs.size(), 0.0);
-  if (bs.empty()) return TOPT_OK;
-  int np = 0;
-  launch_multidot(a, bs.data(), (int)bs.size(), c->vecN, c->partials, &np, st);
-  launch_finalize_multi(c->partials, 0, (int)bs.size(), np, 1.0, c->dots, st);
+  const int n = (int)bs.size();
+  out.assign(n, 0.0);
+  if (n == 0) return TOPT_OK;
+  std::vector<double*> dd;
+  for (auto& sl : c->slabs) {
+    std::vector<const float*> b;
+    for (auto& f : bs) b.push_back(f(sl));
+    int np = 0;
+    launch_multidot(a(sl), b.data(), n, c->vecN, sl.partials, &np, st);
+    launch_finalize_multi(sl.partials, 0, n, np, 1.0, sl.dots, st);
+    dd.push_back(sl.dots);
+  }
+  comm_allreduce(c, dd, n, false, st);
   TOPT_CHECK_LAUNCH();
-  TOPT_CUDA(cudaMemcpyAsync(out.data(), c->dots, bs.size() * 8, cudaMemcpyDeviceToHost, st));
+  TOPT_CUDA(cudaMemcpyAsync(out.data(), c->slabs[0].dots, n * 8, cudaMemcpyDeviceToHost, st));
   TOPT_CUDA(cudaStreamSynchronize(st));
   return TOPT_OK;
 }
 
-// in-place Leray projection of a vector field (b-chain with b := x, assemble writes P_L x)
-void leray_inplace(topt_ctx* c, float* x, cudaStream_t st) {
-  launch_bchain(c->g, x, c->Z, c->p.alpha, c->p.reg_order, true, st);
-  int np = 0;
-  launch_assemble(c->g, c->Z, true, nullptr, nullptr, nullptr, nullptr, x, nullptr, c->partials, &np, st);
+// in-place Leray projection of a per-slab vector field (b-chain with b := x; assemble -> P_L x)
+void leray_inplace(topt_ctx* c, std::function<float*(Slab&)> x, cudaStream_t st) {
+  const int P = P_of(c);
+  const size_t F = c->F;
+  const int bin = bchain_nin(c->slabs[0].g, true), bout = bchain_nout(c->slabs[0].g, true);
+  for (auto& sl : c->slabs) {
+    float2* Z[4] = {sl.Z, sl.Z + F, sl.Z + 2 * F, sl.Z + 3 * F};
+    bchain_xy(sl.g, x(sl), Z, true, st);
+  }
+  if (P > 1)
+    for (int f = 0; f < bin; ++f) {
+      std::vector<float2*> a, b;
+      for (auto& sl : c->slabs) { a.push_back(sl.Z + f * F); b.push_back(sl.Zy + f * F); }
+      tz2y(c, a, b, st);
+    }
+  for (auto& sl : c->slabs) {
+    float2* base = P > 1 ? sl.Zy : sl.Z;
+    float2* Z[4] = {base, base + F, base + 2 * F, base + 3 * F};
+    bchain_last(P > 1 ? sl.gy : sl.g, Z, c->p.alpha, c->p.reg_order, true, ntot(c), st);
+  }
+  if (P > 1)
+    for (int f = 0; f < bout; ++f) {
+      std::vector<float2*> a, b;
+      for (auto& sl : c->slabs) { a.push_back(sl.Zy + f * F); b.push_back(sl.Z + f * F); }
+      ty2z(c, a, b, st);
+    }
+  for (auto& sl : c->slabs) {
+    float2* Z[4] = {sl.Z, sl.Z + F, sl.Z + 2 * F, sl.Z + 3 * F};
+    bchain_yinv(sl.g, Z, true, st);
+    int np = 0;
+    launch_assemble(sl.g, sl.Z, true, nullptr, nullptr, nullptr, nullptr, x(sl), nullptr, sl.partials, &np, st);
+  }
 }
 
 double now() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// Emulated z-slabs: the caller passes whole-grid arrays; slab s of a scalar field is the
+// contiguous block s*F, of component c of a vector field the block c*F_all + s*F.
+bool emu(const topt_ctx* c) { return c->comm.P > 1 && c->comm.emulated(); }
+
+void stage_vec_in(topt_ctx* c, const float* full, std::function<float*(Slab&)> dst, cudaStream_t st) {
+  const size_t F = c->F, Fall = F * c->comm.P;
+  for (size_t si = 0; si < c->slabs.size(); ++si)
+    for (int a = 0; a < c->d; ++a)
+      cudaMemcpyAsync(dst(c->slabs[si]) + a * F, full + a * Fall + si * F, F * 4, cudaMemcpyDeviceToDevice, st);
+}
+void stage_vec_out(topt_ctx* c, std::function<const float*(Slab&)> src, float* full, cudaStream_t st) {
+  const size_t F = c->F, Fall = F * c->comm.P;
+  for (size_t si = 0; si < c->slabs.size(); ++si)
+    for (int a = 0; a < c->d; ++a)
+      cudaMemcpyAsync(full + a * Fall + si * F, src(c->slabs[si]) + a * F, F * 4, cudaMemcpyDeviceToDevice, st);
+}
+
+// Build the per-slab Io of an evaluation at user pointers (emulation: staged copies).
+std::vector<Io> make_io(topt_ctx* c, const float* m0, const float* m1, const float* v, int set, cudaStream_t st) {
+  std::vector<Io> io(c->slabs.size());
+  if (emu(c)) stage_vec_in(c, v, [](Slab& s) { return s.vb; }, st);
+  for (size_t si = 0; si < c->slabs.size(); ++si) {
+    Slab& sl = c->slabs[si];
+    io[si].m0 = emu(c) ? m0 + si * sl.F : m0;
+    io[si].m1 = emu(c) ? m1 + si * sl.F : m1;
+    io[si].v = emu(c) ? sl.vb : v;
+    io[si].u = nullptr;
+    io[si].g = sl.gcur;
+    io[si].s = sl.scur;
+    io[si].scal = sl.pub(set);
+    io[si].isc = sl.intl(set);
+  }
+  return io;
 }
 
 }  // namespace
@@ -570,7 +842,22 @@ topt_status topt_eval_gradient(topt_ctx* c, const float* m0, const float* m1, co
   if (!m0 || !m1 || !v || !d_scalars) return fail(TOPT_ERR_INVALID_ARG, "NULL argument");
   if (!aligned16(m0) || !aligned16(m1) || !aligned16(v) || (g && !aligned16(g)) || (s && !aligned16(s)))
     return fail(TOPT_ERR_INVALID_ARG, "pointers must be 16-byte aligned");
-  return eval_gradient(c, m0, m1, v, nullptr, g, s, d_scalars, intl(c, 4), (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<Io> io = make_io(c, m0, m1, v, 4, st);
+  if (!emu(c)) {
+    io[0].g = g;
+    io[0].s = s;
+    io[0].scal = d_scalars;
+  }
+  topt_status r = eval_gradient(c, io, st);
+  if (r != TOPT_OK) return r;
+  if (emu(c)) {
+    if (g) stage_vec_out(c, [](Slab& x) { return (const float*)x.gcur; }, g, st);
+    if (s) stage_vec_out(c, [](Slab& x) { return (const float*)x.scur; }, s, st);
+    TOPT_CUDA(cudaMemcpyAsync(d_scalars, c->slabs[0].pub(4), TOPT_NSCALARS * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  TOPT_CHECK_LAUNCH();
+  return TOPT_OK;
 }
 
 topt_status topt_eval_gradient_host(topt_ctx* c, const float* m0_h, const float* m1_h, const float* v_h, float* g_h,
@@ -578,14 +865,17 @@ topt_status topt_eval_gradient_host(topt_ctx* c, const float* m0_h, const float*
   topt_status s0 = need_ws(c);
   if (s0 != TOPT_OK) return s0;
   if (!m0_h || !m1_h || !v_h || !h_scalars) return fail(TOPT_ERR_INVALID_ARG, "NULL argument");
+  if (emu(c)) return fail(TOPT_ERR_UNSUPPORTED, "host-buffer evaluation with emulated slabs");
   cudaStream_t st = (cudaStream_t)stream;
-  TOPT_CUDA(cudaMemcpyAsync(c->m0b, m0_h, c->F * 4, cudaMemcpyHostToDevice, st));
-  TOPT_CUDA(cudaMemcpyAsync(c->m1b, m1_h, c->F * 4, cudaMemcpyHostToDevice, st));
-  TOPT_CUDA(cudaMemcpyAsync(c->vb, v_h, c->vecN * 4, cudaMemcpyHostToDevice, st));
-  topt_status r = eval_gradient(c, c->m0b, c->m1b, c->vb, nullptr, c->gcur, c->scur, pub(c, 4), intl(c, 4), st);
+  Slab& sl = c->slabs[0];
+  TOPT_CUDA(cudaMemcpyAsync(sl.m0b, m0_h, c->F * 4, cudaMemcpyHostToDevice, st));
+  TOPT_CUDA(cudaMemcpyAsync(sl.m1b, m1_h, c->F * 4, cudaMemcpyHostToDevice, st));
+  TOPT_CUDA(cudaMemcpyAsync(sl.vb, v_h, c->vecN * 4, cudaMemcpyHostToDevice, st));
+  std::vector<Io> io = make_io(c, sl.m0b, sl.m1b, sl.vb, 4, st);
+  topt_status r = eval_gradient(c, io, st);
   if (r != TOPT_OK) return r;
-  if (g_h) TOPT_CUDA(cudaMemcpyAsync(g_h, c->gcur, c->vecN * 4, cudaMemcpyDeviceToHost, st));
-  TOPT_CUDA(cudaMemcpyAsync(h_scalars, pub(c, 4), TOPT_NSCALARS * 8, cudaMemcpyDeviceToHost, st));
+  if (g_h) TOPT_CUDA(cudaMemcpyAsync(g_h, sl.gcur, c->vecN * 4, cudaMemcpyDeviceToHost, st));
+  TOPT_CUDA(cudaMemcpyAsync(h_scalars, sl.pub(4), TOPT_NSCALARS * 8, cudaMemcpyDeviceToHost, st));
   TOPT_CUDA(cudaStreamSynchronize(st));
   return TOPT_OK;
 }
@@ -596,81 +886,126 @@ topt_status topt_objective(topt_ctx* c, const float* m0, const float* m1, const 
   if (s0 != TOPT_OK) return s0;
   if (!m0 || !m1 || !v || !d_scalars) return fail(TOPT_ERR_INVALID_ARG, "NULL argument");
   cudaStream_t st = (cudaStream_t)stream;
-  forward_half(c, m0, m1, v, false, d_scalars, intl(c, 4), st);
-  // reg = alpha/2 <v, L v>_h = h^d/2 sum v u,  u = alpha L v (fp64 chain)
-  launch_vchain(c->g, v, c->Zv, c->utmp, c->p.alpha, c->p.reg_order, false, st);  // plain L, as in (1.1a)
-  const float* bs[1] = {c->utmp};
-  int np = 0;
-  launch_multidot(v, bs, 1, c->vecN, c->partials, &np, st);
-  launch_finalize_multi(c->partials, 0, 1, np, 0.5 * c->cellvol, d_scalars + TOPT_S_REG, st);
-  launch_combine_obj(d_scalars, st);
+  std::vector<Io> io = make_io(c, m0, m1, v, 4, st);
+  forward_half(c, io, false, st);
+  // reg = alpha/2 <v, L v>_h = h^d/2 sum v u,  u = alpha L v (fp64 chain, plain L as in (1.1a))
+  const int P = P_of(c);
+  const size_t F = c->F;
+  for (size_t si = 0; si < c->slabs.size(); ++si) {
+    Slab& sl = c->slabs[si];
+    double2* Z[3] = {sl.Zv, sl.Zv + F, sl.Zv + 2 * F};
+    vchain_xy(sl.g, io[si].v, Z, false, st);
+  }
+  const int vin = vchain_nin(c->slabs[0].g, false), vout = vchain_nout(c->slabs[0].g);
+  if (P > 1)
+    for (int f = 0; f < vin; ++f) {
+      std::vector<double2*> a, b;
+      for (auto& sl : c->slabs) { a.push_back(sl.Zv + f * F); b.push_back(sl.Zvy + f * F); }
+      tz2y(c, a, b, st);
+    }
+  for (auto& sl : c->slabs) {
+    double2* base = P > 1 ? sl.Zvy : sl.Zv;
+    double2* Z[3] = {base, base + F, base + 2 * F};
+    vchain_last(P > 1 ? sl.gy : sl.g, Z, c->p.alpha, c->p.reg_order, false, ntot(c), st);
+  }
+  if (P > 1)
+    for (int f = 0; f < vout; ++f) {
+      std::vector<double2*> a, b;
+      for (auto& sl : c->slabs) { a.push_back(sl.Zvy + f * F); b.push_back(sl.Zv + f * F); }
+      ty2z(c, a, b, st);
+    }
+  std::vector<double*> regs;
+  for (size_t si = 0; si < c->slabs.size(); ++si) {
+    Slab& sl = c->slabs[si];
+    double2* Z[3] = {sl.Zv, sl.Zv + F, sl.Zv + 2 * F};
+    vchain_inv(sl.g, Z, sl.utmp, st);
+    const float* bs[1] = {sl.utmp};
+    int np = 0;
+    launch_multidot(io[si].v, bs, 1, c->vecN, sl.partials, &np, st);
+    launch_finalize_multi(sl.partials, 0, 1, np, 0.5 * c->cellvol, io[si].scal + TOPT_S_REG, st);
+    regs.push_back(io[si].scal + TOPT_S_REG);
+  }
+  comm_allreduce(c, regs, 1, false, st);
+  for (auto& x : io) launch_combine_obj(x.scal, st);
+  TOPT_CUDA(cudaMemcpyAsync(d_scalars, io[0].scal, TOPT_NSCALARS * 8, cudaMemcpyDeviceToDevice, st));
   TOPT_CHECK_LAUNCH();
   return TOPT_OK;
 }
 
-topt_status topt_feet(topt_ctx* c, const float* v, float* delta_f, float* delta_a, void* stream) {
+static topt_status single_slab(topt_ctx* c) {
   topt_status s0 = need_ws(c);
   if (s0 != TOPT_OK) return s0;
+  if (c->comm.P != 1) return fail(TOPT_ERR_UNSUPPORTED, "per-operator entry points run on one slab (world == 1)");
+  return TOPT_OK;
+}
+
+topt_status topt_feet(topt_ctx* c, const float* v, float* delta_f, float* delta_a, void* stream) {
+  topt_status s0 = single_slab(c);
+  if (s0 != TOPT_OK) return s0;
   if (!v || (!delta_f && !delta_a)) return fail(TOPT_ERR_INVALID_ARG, "NULL argument");
-  launch_trace(c->g, v, delta_f, delta_a, nullptr, nullptr, (cudaStream_t)stream);
+  launch_trace(c->slabs[0].g, v, delta_f, delta_a, nullptr, nullptr, (cudaStream_t)stream);
   TOPT_CHECK_LAUNCH();
   return TOPT_OK;
 }
 
 topt_status topt_forward(topt_ctx* c, const float* m0, const float* v, float* m_traj, void* stream) {
-  topt_status s0 = need_ws(c);
+  topt_status s0 = single_slab(c);
   if (s0 != TOPT_OK) return s0;
   if (!m0 || !v || !m_traj) return fail(TOPT_ERR_INVALID_ARG, "NULL argument");
   cudaStream_t st = (cudaStream_t)stream;
-  forward_half(c, m0, m0, v, false, pub(c, 4), intl(c, 4), st);
-  TOPT_CUDA(cudaMemcpyAsync(m_traj, c->m_traj, (c->p.nt + 1) * c->F * 4, cudaMemcpyDeviceToDevice, st));
+  std::vector<Io> io = make_io(c, m0, m0, v, 4, st);
+  forward_half(c, io, false, st);
+  TOPT_CUDA(cudaMemcpyAsync(m_traj, c->slabs[0].m_traj, (c->p.nt + 1) * c->F * 4, cudaMemcpyDeviceToDevice, st));
   TOPT_CHECK_LAUNCH();
   return TOPT_OK;
 }
 
 topt_status topt_get_adjoint(topt_ctx* c, float* lam_traj, float* body_force, void* stream) {
-  topt_status s0 = need_ws(c);
+  topt_status s0 = single_slab(c);
   if (s0 != TOPT_OK) return s0;
   cudaStream_t st = (cudaStream_t)stream;
   if (lam_traj)
-    TOPT_CUDA(cudaMemcpyAsync(lam_traj, c->lam_traj, (c->p.nt + 1) * c->F * 4, cudaMemcpyDeviceToDevice, st));
-  if (body_force) TOPT_CUDA(cudaMemcpyAsync(body_force, c->b, c->vecN * 4, cudaMemcpyDeviceToDevice, st));
+    TOPT_CUDA(cudaMemcpyAsync(lam_traj, c->slabs[0].lam_traj, (c->p.nt + 1) * c->F * 4, cudaMemcpyDeviceToDevice,
+                              st));
+  if (body_force) TOPT_CUDA(cudaMemcpyAsync(body_force, c->slabs[0].b, c->vecN * 4, cudaMemcpyDeviceToDevice, st));
   return TOPT_OK;
 }
 
 topt_status topt_derivative(topt_ctx* c, const float* f, int32_t axis, float* out, void* stream) {
-  topt_status s0 = need_ws(c);
+  topt_status s0 = single_slab(c);
   if (s0 != TOPT_OK) return s0;
   if (!f || !out) return fail(TOPT_ERR_INVALID_ARG, "NULL argument");
   if (axis < 0 || axis >= c->d) return fail(TOPT_ERR_INVALID_ARG, "axis out of range");
   double one = 1.0;
   DerivArgs da{f, 0, nullptr, 0, &one, 1, 0.f, out};
-  launch_deriv_accum(c->g, axis, da, (cudaStream_t)stream);
+  launch_deriv_accum(c->slabs[0].g, axis, da, (cudaStream_t)stream);
   TOPT_CHECK_LAUNCH();
   return TOPT_OK;
 }
 
 topt_status topt_apply_precond(topt_ctx* c, const float* g, float* s, void* stream) {
-  topt_status s0 = need_ws(c);
+  topt_status s0 = single_slab(c);
   if (s0 != TOPT_OK) return s0;
   if (!g || !s) return fail(TOPT_ERR_INVALID_ARG, "NULL argument");
   cudaStream_t st = (cudaStream_t)stream;
+  Slab& sl = c->slabs[0];
   const bool leray = c->p.model == TOPT_INCOMPRESSIBLE;
-  launch_bchain(c->g, g, c->Z, c->p.alpha, c->p.reg_order, leray, st);
+  launch_bchain(sl.g, g, sl.Z, c->p.alpha, c->p.reg_order, leray, st);
   int np = 0;
-  launch_assemble(c->g, c->Z, leray, g, nullptr, nullptr, nullptr, nullptr, s, c->partials, &np, st);
+  launch_assemble(sl.g, sl.Z, leray, g, nullptr, nullptr, nullptr, nullptr, s, sl.partials, &np, st);
   TOPT_CHECK_LAUNCH();
   return TOPT_OK;
 }
 
 topt_status topt_leray(topt_ctx* c, const float* u, float* out, void* stream) {
-  topt_status s0 = need_ws(c);
+  topt_status s0 = single_slab(c);
   if (s0 != TOPT_OK) return s0;
   if (!u || !out) return fail(TOPT_ERR_INVALID_ARG, "NULL argument");
   cudaStream_t st = (cudaStream_t)stream;
-  launch_bchain(c->g, u, c->Z, c->p.alpha, c->p.reg_order, true, st);
+  Slab& sl = c->slabs[0];
+  launch_bchain(sl.g, u, sl.Z, c->p.alpha, c->p.reg_order, true, st);
   int np = 0;
-  launch_assemble(c->g, c->Z, true, nullptr, nullptr, nullptr, nullptr, out, nullptr, c->partials, &np, st);
+  launch_assemble(sl.g, sl.Z, true, nullptr, nullptr, nullptr, nullptr, out, nullptr, sl.partials, &np, st);
   TOPT_CHECK_LAUNCH();
   return TOPT_OK;
 }
@@ -679,11 +1014,15 @@ topt_status topt_multidot(topt_ctx* c, const float* a, const float* const* bs, i
                           void* stream) {
   topt_status s0 = need_ws(c);
   if (s0 != TOPT_OK) return s0;
+  if (emu(c)) return fail(TOPT_ERR_UNSUPPORTED, "multidot with emulated slabs");
   if (!a || !bs || !d_dots || count < 1 || count > kMaxVecs) return fail(TOPT_ERR_INVALID_ARG, "bad argument");
   cudaStream_t st = (cudaStream_t)stream;
+  Slab& sl = c->slabs[0];
   int np = 0;
-  launch_multidot(a, bs, count, c->vecN, c->partials, &np, st);
-  launch_finalize_multi(c->partials, 0, count, np, 1.0, d_dots, st);
+  launch_multidot(a, bs, count, c->vecN, sl.partials, &np, st);
+  launch_finalize_multi(sl.partials, 0, count, np, 1.0, d_dots, st);
+  std::vector<double*> dd{d_dots};
+  comm_allreduce(c, dd, count, false, st);
   TOPT_CHECK_LAUNCH();
   return TOPT_OK;
 }
@@ -692,6 +1031,7 @@ topt_status topt_mix(topt_ctx* c, const float* q, const float* const* vs, const 
                      float* out, void* stream) {
   topt_status s0 = need_ws(c);
   if (s0 != TOPT_OK) return s0;
+  if (emu(c)) return fail(TOPT_ERR_UNSUPPORTED, "mix with emulated slabs");
   if (!q || !out || count < 0 || count > kMaxVecs || (count && (!vs || !beta)))
     return fail(TOPT_ERR_INVALID_ARG, "bad argument");
   launch_mix(q, vs, beta, count, c->vecN, out, (cudaStream_t)stream);
@@ -742,6 +1082,7 @@ topt_status topt_set_step_replay(topt_ctx* c, const double* rho, int32_t count) 
 // GA-NGMRES(w; sigma, tau) (Alg. 3) / GA-AA, host-driven.  u = alpha L v is carried with
 // every iterate (q: u_q = u - rho P_0 g since alpha L s = -P_0 g; mixing is linear), so the
 // evaluations inside the solve never apply L to a stored fp32 field.
+// Every vector operation runs on every local slab; inner products are all-reduced.
 topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_inout, topt_report* rep,
                        void* stream) {
   topt_status s0 = need_ws(c);
@@ -753,18 +1094,38 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
   const int W1 = P.window + 1;
   const bool aa = P.method == TOPT_GA_AA;
   const bool leray = P.model == TOPT_INCOMPRESSIBLE;
-  const double nF = (double)c->F;
+  const double nF = ntot(c);
+  const size_t nsl = c->slabs.size();
   std::memset(rep, 0, sizeof(*rep));
   const double t0 = now();
   double t_pde = 0.0, t_ls = 0.0;
   int grad_evals = 0, obj_evals = 0, nsteps = 0;
   std::deque<double> replay(c->replay.begin(), c->replay.end());
   topt_status r;
+  using Acc = std::function<float*(Slab&)>;
+  using CAcc = std::function<const float*(Slab&)>;
+
+  // per-slab problem data (emulation: the user's whole-grid arrays are sliced)
+  std::vector<const float*> m0s(nsl), m1s(nsl);
+  for (size_t si = 0; si < nsl; ++si) {
+    m0s[si] = emu(c) ? m0 + si * c->F : m0;
+    m1s[si] = emu(c) ? m1 + si * c->F : m1;
+  }
+  auto io_at = [&](Acc v, Acc u, Acc g, Acc s, int set) {
+    std::vector<Io> io(nsl);
+    for (size_t si = 0; si < nsl; ++si) {
+      Slab& sl = c->slabs[si];
+      io[si] = Io{m0s[si], m1s[si], v(sl), u ? u(sl) : nullptr, g ? g(sl) : nullptr, s ? s(sl) : nullptr,
+                  sl.pub(set), sl.intl(set)};
+    }
+    return io;
+  };
 
   // history slot i: A = v (AA: r), B = g (AA: q), U = u (AA: u(q))
-  auto slotA = [&](int i) { return c->hist + (size_t)(3 * i) * V; };
-  auto slotB = [&](int i) { return c->hist + (size_t)(3 * i + 1) * V; };
-  auto slotU = [&](int i) { return c->hist + (size_t)(3 * i + 2) * V; };
+  auto slotA = [&](int i) { return Acc([i, V](Slab& s) { return s.hist + (size_t)(3 * i) * V; }); };
+  auto slotB = [&](int i) { return Acc([i, V](Slab& s) { return s.hist + (size_t)(3 * i + 1) * V; }); };
+  auto slotU = [&](int i) { return Acc([i, V](Slab& s) { return s.hist + (size_t)(3 * i + 2) * V; }); };
+  auto cacc = [](Acc a) { return CAcc([a](Slab& s) { return (const float*)a(s); }); };
   std::deque<int> win;  // ring slots, most recent last
   std::vector<std::vector<double>> H(W1, std::vector<double>(W1, 0.0));  // <B_i, B_j> by slot
   auto take_slot = [&]() {
@@ -777,74 +1138,99 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
     }
     return slot;
   };
+  auto copyv = [&](Acc dst, Acc src) {
+    for (auto& sl : c->slabs) cudaMemcpyAsync(dst(sl), src(sl), V * 4, cudaMemcpyDeviceToDevice, st);
+  };
   // push (a, b, u) and refresh the Gram row of b against the window
-  auto push = [&](const float* a, const float* b, const float* u, bool gram) -> topt_status {
+  auto push = [&](Acc a, Acc b, Acc u, bool gram) -> topt_status {
     const int slot = take_slot();
-    TOPT_CUDA(cudaMemcpyAsync(slotA(slot), a, V * 4, cudaMemcpyDeviceToDevice, st));
-    TOPT_CUDA(cudaMemcpyAsync(slotB(slot), b, V * 4, cudaMemcpyDeviceToDevice, st));
-    TOPT_CUDA(cudaMemcpyAsync(slotU(slot), u, V * 4, cudaMemcpyDeviceToDevice, st));
+    copyv(slotA(slot), a);
+    copyv(slotB(slot), b);
+    copyv(slotU(slot), u);
     win.push_back(slot);
     if (!gram) return TOPT_OK;
-    std::vector<const float*> bs;
-    for (int s2 : win) bs.push_back(slotB(s2));
+    std::vector<CAcc> bs;
+    for (int s2 : win) bs.push_back(cacc(slotB(s2)));
     std::vector<double> dd;
-    topt_status rr = host_dots(c, slotB(slot), bs, dd, st);
+    topt_status rr = host_dots(c, cacc(slotB(slot)), bs, dd, st);
     if (rr != TOPT_OK) return rr;
     for (size_t i = 0; i < win.size(); ++i) H[slot][win[i]] = H[win[i]][slot] = dd[i];
     return TOPT_OK;
   };
+  Acc Vc = [](Slab& s) { return s.vcur; }, Uc = [](Slab& s) { return s.ucur; };
+  Acc Gc = [](Slab& s) { return s.gcur; }, Sc = [](Slab& s) { return s.scur; };
+  Acc Q = [](Slab& s) { return s.q; }, Uq = [](Slab& s) { return s.uq; };
+  Acc Gq = [](Slab& s) { return s.gq; }, Sq = [](Slab& s) { return s.sq; };
+  Acc Vn = [](Slab& s) { return s.vnew; }, Un = [](Slab& s) { return s.unew; };
+  Acc Gn = [](Slab& s) { return s.gnew; }, Sn = [](Slab& s) { return s.snew; };
+  Acc Vt = [](Slab& s) { return s.vt; };
 
   // v^0, u^0 = alpha L v^0 (fp64 chain, once), g(v^0)
-  TOPT_CUDA(cudaMemcpyAsync(c->vcur, v_inout, V * 4, cudaMemcpyDeviceToDevice, st));
-  if (leray) leray_inplace(c, c->vcur, st);
-  launch_vchain(c->g, c->vcur, c->Zv, c->ucur, P.alpha, P.reg_order, leray, st);
+  if (emu(c)) stage_vec_in(c, v_inout, Vc, st);
+  else TOPT_CUDA(cudaMemcpyAsync(c->slabs[0].vcur, v_inout, V * 4, cudaMemcpyDeviceToDevice, st));
+  if (leray) leray_inplace(c, Vc, st);
   double te = now();
-  if ((r = eval_gradient(c, m0, m1, c->vcur, c->ucur, c->gcur, c->scur, pub(c, 0), intl(c, 0), st)) != TOPT_OK)
-    return r;
+  {
+    std::vector<Io> io = io_at(Vc, nullptr, Gc, Sc, 0);
+    forward_half(c, io, true, st);
+    backward_half(c, io, st);  // computes u = alpha L v^0 into utmp
+    for (auto& sl : c->slabs) cudaMemcpyAsync(sl.ucur, sl.utmp, V * 4, cudaMemcpyDeviceToDevice, st);
+    TOPT_CHECK_LAUNCH();
+  }
   ++grad_evals;
   HostScalars cur, qs, ns;
   if ((r = fetch(c, 0, cur, st)) != TOPT_OK) return r;
   t_pde += now() - te;
   const double g0 = cur.pub(TOPT_S_GRAD_INF);
   rep->grad_inf0 = g0;
-  if (!aa && (r = push(c->vcur, c->gcur, c->ucur, true)) != TOPT_OK) return r;
+  if (!aa && (r = push(Vc, Gc, Uc, true)) != TOPT_OK) return r;
 
   // q-state helpers: v_q = v + rho s, u_q = u - rho (g - gbar)
   auto make_q = [&](double rho_) {
-    launch_axpy(c->vcur, (float)rho_, c->scur, V, c->q, st);
     float cst[3] = {0.f, 0.f, 0.f};
     for (int a = 0; a < c->d; ++a) cst[a] = (float)(rho_ * cur.in(I_SUMG + a) / nF);
-    launch_axpy_c(c->ucur, (float)(-rho_), c->gcur, V, c->d, cst, c->uq, st);
+    for (auto& sl : c->slabs) {
+      launch_axpy(sl.vcur, (float)rho_, sl.scur, V, sl.q, st);
+      launch_axpy_c(sl.ucur, (float)(-rho_), sl.gcur, V, c->d, cst, sl.uq, st);
+    }
   };
-  auto eval_q = [&]() -> topt_status {
-    topt_status rr = eval_gradient(c, m0, m1, c->q, c->uq, c->gq, c->sq, pub(c, 2), intl(c, 2), st);
+  auto eval_into = [&](Acc v, Acc u, Acc g, Acc s, int set, HostScalars& out) -> topt_status {
+    std::vector<Io> io = io_at(v, u, g, s, set);
+    topt_status rr = eval_gradient(c, io, st);
     if (rr != TOPT_OK) return rr;
     ++grad_evals;
-    return fetch(c, 2, qs, st);
+    return fetch(c, set, out, st);
+  };
+  auto rotate = [&](float* Slab::*a, float* Slab::*b) {
+    for (auto& sl : c->slabs) std::swap(sl.*a, sl.*b);
   };
   auto accept_q = [&]() {
-    std::swap(c->vcur, c->q);
-    std::swap(c->ucur, c->uq);
-    std::swap(c->gcur, c->gq);
-    std::swap(c->scur, c->sq);
+    rotate(&Slab::vcur, &Slab::q);
+    rotate(&Slab::ucur, &Slab::uq);
+    rotate(&Slab::gcur, &Slab::gq);
+    rotate(&Slab::scur, &Slab::sq);
     cur = qs;
   };
   auto eval_new = [&]() -> topt_status {
     if (leray) {
-      leray_inplace(c, c->vnew, st);
-      leray_inplace(c, c->unew, st);
+      leray_inplace(c, Vn, st);
+      leray_inplace(c, Un, st);
     }
-    topt_status rr = eval_gradient(c, m0, m1, c->vnew, c->unew, c->gnew, c->snew, pub(c, 3), intl(c, 3), st);
+    topt_status rr = eval_into(Vn, Un, Gn, Sn, 3, ns);
     if (rr != TOPT_OK) return rr;
-    ++grad_evals;
-    rr = fetch(c, 3, ns, st);
-    if (rr != TOPT_OK) return rr;
-    std::swap(c->vcur, c->vnew);
-    std::swap(c->ucur, c->unew);
-    std::swap(c->gcur, c->gnew);
-    std::swap(c->scur, c->snew);
+    rotate(&Slab::vcur, &Slab::vnew);
+    rotate(&Slab::ucur, &Slab::unew);
+    rotate(&Slab::gcur, &Slab::gnew);
+    rotate(&Slab::scur, &Slab::snew);
     cur = ns;
     return TOPT_OK;
+  };
+  auto mix_into = [&](Acc out, Acc q, const std::vector<Acc>& vs, const std::vector<double>& beta) {
+    for (auto& sl : c->slabs) {
+      std::vector<const float*> p;
+      for (auto& f : vs) p.push_back(f(sl));
+      launch_mix(q(sl), p.data(), beta.data(), (int)p.size(), V, out(sl), st);
+    }
   };
 
   double rho = 1.0;
@@ -865,7 +1251,9 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
     } else {
       for (int t = 0; t <= P.max_backtracks; ++t) {
         make_q(rho_t);
-        if ((r = trial_dist(c, m0, m1, c->q, pub(c, 1), intl(c, 1), st)) != TOPT_OK) return r;
+        std::vector<Io> io = io_at(Q, nullptr, nullptr, nullptr, 1);
+        forward_half(c, io, false, st);
+        TOPT_CHECK_LAUNCH();
         ++obj_evals;
         HostScalars ts;
         if ((r = fetch(c, 1, ts, st)) != TOPT_OK) return r;
@@ -881,19 +1269,18 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
         rho_t *= 0.5;
       }
     }
+    t_pde += now() - te;
     if (!accepted) {
       exit_code = TOPT_STAGNATED;
-      t_pde += now() - te;
       break;
     }
-    t_pde += now() - te;
 
     const int period = P.sigma + P.tau;
     const bool fp_step = P.ordering == TOPT_ORDER_GA ? (k % period >= P.sigma) : (k % period < P.tau);
     const int wk = std::min(k, P.window);
     if (!aa) {
       te = now();
-      if ((r = eval_q()) != TOPT_OK) return r;  // g(q): both branches need it (R17)
+      if ((r = eval_into(Q, Uq, Gq, Sq, 2, qs)) != TOPT_OK) return r;  // g(q): both branches (R17)
       t_pde += now() - te;
       if (fp_step) {
         accept_q();
@@ -902,11 +1289,11 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
         // fp64 Gram: G_ij = <g_q,g_q> - <g_q,g_i> - <g_q,g_j> + <g_i,g_j>, rhs_i = <C_i, g_q>
         const double tl = now();
         const int m = (int)win.size();  // == w_k + 1
-        std::vector<const float*> bs;
-        for (int i = 0; i < m; ++i) bs.push_back(slotB(win[m - 1 - i]));  // i = 0 -> v^k
-        bs.push_back(c->gq);
+        std::vector<CAcc> bs;
+        for (int i = 0; i < m; ++i) bs.push_back(cacc(slotB(win[m - 1 - i])));  // i = 0 -> v^k
+        bs.push_back(cacc(Gq));
         std::vector<double> rd;
-        if ((r = host_dots(c, c->gq, bs, rd, st)) != TOPT_OK) return r;
+        if ((r = host_dots(c, cacc(Gq), bs, rd, st)) != TOPT_OK) return r;
         const double gam = rd[m];
         std::vector<double> G(m * m), rhs(m);
         for (int i = 0; i < m; ++i) {
@@ -917,59 +1304,59 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
         std::vector<double> beta = lsq_from_gram(m, G, rhs);
         t_ls += now() - tl;
         // v^{k+1} = q + sum beta_i (q - v^{k-i})  (Alg. 3 line 9), same combination for u
-        std::vector<const float*> vs, us;
+        std::vector<Acc> vs, us;
         for (int i = 0; i < m; ++i) {
           vs.push_back(slotA(win[m - 1 - i]));
           us.push_back(slotU(win[m - 1 - i]));
         }
-        launch_mix(c->q, vs.data(), beta.data(), m, V, c->vnew, st);
-        launch_mix(c->uq, us.data(), beta.data(), m, V, c->unew, st);
+        mix_into(Vn, Q, vs, beta);
+        mix_into(Un, Uq, us, beta);
         te = now();
         if ((r = eval_new()) != TOPT_OK) return r;
         t_pde += now() - te;
         ++nsteps;
       }
       (void)wk;
-      if ((r = push(c->vcur, c->gcur, c->ucur, true)) != TOPT_OK) return r;
+      if ((r = push(Vc, Gc, Uc, true)) != TOPT_OK) return r;
     } else {
       // AA (Alg. 2): r_k = v^k - q(v^k); LSQ over r_k - r_{k-i}, i = 1..w_k; mix q-images
-      launch_sub(c->vcur, c->q, V, c->vt, st);  // r_k
+      for (auto& sl : c->slabs) launch_sub(sl.vcur, sl.q, V, sl.vt, st);  // r_k
       const int m = std::min((int)win.size(), wk);
       if (!fp_step && m > 0) {
         const double tl = now();
-        std::vector<const float*> bs;
-        for (int i = 0; i < m; ++i) bs.push_back(slotA(win[win.size() - 1 - i]));
-        bs.push_back(c->vt);
+        std::vector<CAcc> bs;
+        for (int i = 0; i < m; ++i) bs.push_back(cacc(slotA(win[win.size() - 1 - i])));
+        bs.push_back(cacc(Vt));
         std::vector<double> rd;
-        if ((r = host_dots(c, c->vt, bs, rd, st)) != TOPT_OK) return r;
+        if ((r = host_dots(c, cacc(Vt), bs, rd, st)) != TOPT_OK) return r;
         const double gam = rd[m];
         std::vector<double> G(m * m), rhs(m);
         for (int i = 0; i < m; ++i) {
-          std::vector<const float*> b2;
-          for (int j = 0; j < m; ++j) b2.push_back(slotA(win[win.size() - 1 - j]));
+          std::vector<CAcc> b2;
+          for (int j = 0; j < m; ++j) b2.push_back(cacc(slotA(win[win.size() - 1 - j])));
           std::vector<double> row;
-          if ((r = host_dots(c, slotA(win[win.size() - 1 - i]), b2, row, st)) != TOPT_OK) return r;
+          if ((r = host_dots(c, cacc(slotA(win[win.size() - 1 - i])), b2, row, st)) != TOPT_OK) return r;
           rhs[i] = gam - rd[i];
           for (int j = 0; j < m; ++j) G[i * m + j] = gam - rd[i] - rd[j] + row[j];
         }
         std::vector<double> xi = lsq_from_gram(m, G, rhs);
         t_ls += now() - tl;
-        std::vector<const float*> qv, qu;
+        std::vector<Acc> qv, qu;
         for (int i = 0; i < m; ++i) {
           qv.push_back(slotB(win[win.size() - 1 - i]));
           qu.push_back(slotU(win[win.size() - 1 - i]));
         }
-        launch_mix(c->q, qv.data(), xi.data(), m, V, c->vnew, st);
-        launch_mix(c->uq, qu.data(), xi.data(), m, V, c->unew, st);
-        if ((r = push(c->vt, c->q, c->uq, false)) != TOPT_OK) return r;
+        mix_into(Vn, Q, qv, xi);
+        mix_into(Un, Uq, qu, xi);
+        if ((r = push(Vt, Q, Uq, false)) != TOPT_OK) return r;
         te = now();
         if ((r = eval_new()) != TOPT_OK) return r;
         t_pde += now() - te;
         ++nsteps;
       } else {
-        if ((r = push(c->vt, c->q, c->uq, false)) != TOPT_OK) return r;
+        if ((r = push(Vt, Q, Uq, false)) != TOPT_OK) return r;
         te = now();
-        if ((r = eval_q()) != TOPT_OK) return r;
+        if ((r = eval_into(Q, Uq, Gq, Sq, 2, qs)) != TOPT_OK) return r;
         t_pde += now() - te;
         accept_q();
       }
@@ -987,7 +1374,8 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
       break;
     }
   }
-  TOPT_CUDA(cudaMemcpyAsync(v_inout, c->vcur, V * 4, cudaMemcpyDeviceToDevice, st));
+  if (emu(c)) stage_vec_out(c, cacc(Vc), v_inout, st);
+  else TOPT_CUDA(cudaMemcpyAsync(v_inout, c->slabs[0].vcur, V * 4, cudaMemcpyDeviceToDevice, st));
   TOPT_CUDA(cudaStreamSynchronize(st));
   rep->obj = cur.pub(TOPT_S_OBJ);
   rep->dist = cur.pub(TOPT_S_DIST);

@@ -1,0 +1,86 @@
+// ctx.cuh — library context: per-slab state and the z-slab communicator (not part of the ABI).
+//
+// z-slab decomposition (BASELINE north_star): the 3D grid is cut into P slabs of
+// nz/P planes.  Each slab owns its fields; interpolated inputs carry zh = 4 halo planes per
+// side (ring-periodic neighbour exchange before every SL step), z-derivatives and the z passes
+// of the 3D FFTs run in a y-slab layout [nz][ny/P][nx] reached by an all-to-all transpose, and
+// reductions are all-reduced.  One process may hold every slab (emulation on one GPU: the
+// exchanges are device copies — used to test P-invariance) or exactly one (NCCL over NVLink).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+#ifdef TOPT_WITH_NCCL
+#include <nccl.h>
+#endif
+
+namespace topt {
+
+constexpr int kSet = 32;  // doubles per scalar set: [0, 16) public, [16, 32) internal
+constexpr int kSlabHalo = 4;
+
+struct Slab {
+  int index = 0;   // global slab index (rank)
+  Geom g{};        // z-slab geometry (nz = local planes; zh = halo when P > 1)
+  Geom gy{};       // y-slab geometry of the z passes (P > 1)
+  size_t F = 0;    // local points
+  size_t Fh = 0;   // local points incl. halo planes
+  size_t plane = 0;
+  float *m_traj{}, *lam_traj{}, *vh{}, *divv{};  // halo'd (Fh per slice / component)
+  float *df{}, *da{}, *E{}, *b{}, *utmp{};
+  float2* Z{};     // b-chain: 4 complex fields of F
+  double2* Zv{};   // v-chain: 3 double-complex fields of F
+  float2* Zy{};    // y-slab copies for P > 1
+  double2* Zvy{};
+  float* ytraj{};  // y-slab copies of the S+1 state and adjoint slices (P > 1)
+  float* ytmp{};   // y-slab scratch (F)
+  char* sendbuf{}; // NCCL transpose packing (16 F bytes)
+  float *m0b{}, *m1b{}, *vb{}, *vt{};
+  float *vcur{}, *gcur{}, *scur{}, *q{}, *gq{}, *sq{}, *vnew{}, *gnew{}, *snew{};
+  float *ucur{}, *uq{}, *unew{};
+  float* hist{};
+  double* partials{};
+  double* sc{};    // 5 sets of kSet
+  double* dots{};
+  int* haloerr{};
+  double* pub(int set) const { return sc + set * kSet; }
+  double* intl(int set) const { return sc + set * kSet + 16; }
+};
+
+// Communicator over the P slabs.  nloc == P: all slabs local (device copies); nloc == 1: NCCL.
+struct Comm {
+  int P = 1;
+  int nloc = 1;
+#ifdef TOPT_WITH_NCCL
+  ncclComm_t nccl = nullptr;
+#endif
+  bool emulated() const { return nloc == P; }
+};
+
+}  // namespace topt
+
+struct topt_ctx {
+  topt_params p{};
+  int rank = 0, world = 1, device = 0;
+  int d = 3;
+  int nzg = 1;
+  double h[3]{}, dt = 0, cellvol = 0;
+  std::vector<double> wts;
+  size_t F = 0, vecN = 0;  // per slab
+  char* ws = nullptr;
+  size_t ws_bytes = 0, ws_need = 0, slab_bytes = 0;
+  topt::Comm comm;
+  std::vector<topt::Slab> slabs;
+  std::vector<double> replay;
+  // per-kernel-class timing (topt_profile / topt_kernel_stats)
+  bool prof = false;
+  struct Rec { int cls; cudaEvent_t a, b; double bytes; int launches; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  double pms[16]{}, pbytes[16]{};
+  long long plaunch[16]{};
+};

@@ -1,0 +1,158 @@
+// dist.cu — z-slab communication: halo exchange, z<->y slab transposes, all-reduce.
+//
+// SURVEY §8(e) / BASELINE north_star: "halo exchange over NVLink sized from max|v|*dt for the
+// interpolation, NCCL all-to-all transposes for the distributed FFT, and allreduce for the
+// inner products".  Two transports behind one interface:
+//   * NCCL (one slab per process, one process per GPU): grouped ncclSend/ncclRecv for halos
+//     and the all-to-all, ncclAllReduce for scalars;
+//   * emulation (all P slabs in one process on one GPU): the same data movement as device
+//     copies — used by the tests to check that P slabs reproduce the single-slab result.
+// Layouts: z-slab [nz/P][ny][nx] (halo'd inputs: [zh + nz/P + zh] planes); y-slab
+// [nz][ny/P][nx].  The chunk exchanged between slabs r and q is nz/P x ny/P x nx elements.
+#include <cstdio>
+
+#include "ctx.cuh"
+
+namespace topt {
+
+namespace {
+
+#ifdef TOPT_WITH_NCCL
+bool nccl_ok(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) {
+    fprintf(stderr, "topt: %s failed: %s\n", what, ncclGetErrorString(r));
+    return false;
+  }
+  return true;
+}
+#endif
+
+struct PtrList {
+  double* p[64];
+};
+
+__global__ void k_allreduce_emul(PtrList L, int nslab, int count, int is_max) {
+  const int i = threadIdx.x;
+  if (i >= count) return;
+  double acc = L.p[0][i];
+  for (int s = 1; s < nslab; ++s) acc = is_max ? fmax(acc, L.p[s][i]) : acc + L.p[s][i];
+  for (int s = 0; s < nslab; ++s) L.p[s][i] = acc;
+}
+
+}  // namespace
+
+// Halo planes of nf fields (field f of slab s at base[s] + f * fstride floats, layout
+// [zh + nzl + zh] planes of `plane` floats): low halo <- previous slab's top zh local planes,
+// high halo <- next slab's bottom zh local planes (ring, periodic in z).
+bool comm_halo(topt_ctx* c, const std::vector<float*>& base, int nf, size_t fstride, cudaStream_t st) {
+  const Comm& cm = c->comm;
+  if (cm.P == 1) return true;
+  const Slab& s0 = c->slabs[0];
+  const int zh = s0.g.zh, nzl = s0.g.nz;
+  const size_t pb = s0.plane * sizeof(float), hb = (size_t)zh * pb;
+  if (cm.emulated()) {
+    for (int f = 0; f < nf; ++f)
+      for (int r = 0; r < cm.P; ++r) {
+        const int prev = (r + cm.P - 1) % cm.P, next = (r + 1) % cm.P;
+        float* B = base[r] + f * fstride;
+        cudaMemcpyAsync(B, base[prev] + f * fstride + (size_t)nzl * s0.plane, hb, cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(B + (size_t)(nzl + zh) * s0.plane, base[next] + f * fstride + (size_t)zh * s0.plane, hb,
+                        cudaMemcpyDeviceToDevice, st);
+      }
+    return cudaGetLastError() == cudaSuccess;
+  }
+#ifdef TOPT_WITH_NCCL
+  const int r = c->slabs[0].index, prev = (r + cm.P - 1) % cm.P, next = (r + 1) % cm.P;
+  bool ok = nccl_ok(ncclGroupStart(), "ncclGroupStart");
+  for (int f = 0; f < nf && ok; ++f) {
+    float* B = base[0] + f * fstride;
+    ok &= nccl_ok(ncclSend(B + (size_t)nzl * s0.plane, hb, ncclChar, next, cm.nccl, st), "ncclSend");
+    ok &= nccl_ok(ncclRecv(B, hb, ncclChar, prev, cm.nccl, st), "ncclRecv");
+    ok &= nccl_ok(ncclSend(B + (size_t)zh * s0.plane, hb, ncclChar, prev, cm.nccl, st), "ncclSend");
+    ok &= nccl_ok(ncclRecv(B + (size_t)(nzl + zh) * s0.plane, hb, ncclChar, next, cm.nccl, st), "ncclRecv");
+  }
+  ok &= nccl_ok(ncclGroupEnd(), "ncclGroupEnd");
+  return ok;
+#else
+  return false;
+#endif
+}
+
+// z-slab -> y-slab transpose of one field per slab (element size eb bytes).
+bool comm_z2y(topt_ctx* c, const std::vector<const char*>& src, const std::vector<char*>& dst, size_t eb,
+              cudaStream_t st) {
+  const Comm& cm = c->comm;
+  const Slab& s0 = c->slabs[0];
+  const int P = cm.P, nzl = s0.g.nz, nyl = s0.g.ny / P, nx = s0.g.nx;
+  const size_t w = (size_t)nyl * nx * eb, spitch = (size_t)s0.g.ny * nx * eb, chunk = w * nzl;
+  if (cm.emulated()) {
+    for (int r = 0; r < P; ++r)
+      for (int q = 0; q < P; ++q)
+        cudaMemcpy2DAsync(dst[q] + r * chunk, w, src[r] + q * w, spitch, w, nzl, cudaMemcpyDeviceToDevice, st);
+    return cudaGetLastError() == cudaSuccess;
+  }
+#ifdef TOPT_WITH_NCCL
+  char* sb = c->slabs[0].sendbuf;
+  for (int q = 0; q < P; ++q)
+    cudaMemcpy2DAsync(sb + q * chunk, w, src[0] + q * w, spitch, w, nzl, cudaMemcpyDeviceToDevice, st);
+  bool ok = nccl_ok(ncclGroupStart(), "ncclGroupStart");
+  for (int q = 0; q < P && ok; ++q) {
+    ok &= nccl_ok(ncclSend(sb + q * chunk, chunk, ncclChar, q, cm.nccl, st), "ncclSend");
+    ok &= nccl_ok(ncclRecv(dst[0] + q * chunk, chunk, ncclChar, q, cm.nccl, st), "ncclRecv");
+  }
+  ok &= nccl_ok(ncclGroupEnd(), "ncclGroupEnd");
+  return ok;
+#else
+  return false;
+#endif
+}
+
+// y-slab -> z-slab transpose of one field per slab.
+bool comm_y2z(topt_ctx* c, const std::vector<const char*>& src, const std::vector<char*>& dst, size_t eb,
+              cudaStream_t st) {
+  const Comm& cm = c->comm;
+  const Slab& s0 = c->slabs[0];
+  const int P = cm.P, nzl = s0.g.nz, nyl = s0.g.ny / P, nx = s0.g.nx;
+  const size_t w = (size_t)nyl * nx * eb, dpitch = (size_t)s0.g.ny * nx * eb, chunk = w * nzl;
+  if (cm.emulated()) {
+    for (int r = 0; r < P; ++r)
+      for (int q = 0; q < P; ++q)
+        cudaMemcpy2DAsync(dst[q] + r * w, dpitch, src[r] + q * chunk, w, w, nzl, cudaMemcpyDeviceToDevice, st);
+    return cudaGetLastError() == cudaSuccess;
+  }
+#ifdef TOPT_WITH_NCCL
+  char* rb = c->slabs[0].sendbuf;
+  bool ok = nccl_ok(ncclGroupStart(), "ncclGroupStart");
+  for (int q = 0; q < P && ok; ++q) {
+    ok &= nccl_ok(ncclSend(src[0] + q * chunk, chunk, ncclChar, q, cm.nccl, st), "ncclSend");
+    ok &= nccl_ok(ncclRecv(rb + q * chunk, chunk, ncclChar, q, cm.nccl, st), "ncclRecv");
+  }
+  ok &= nccl_ok(ncclGroupEnd(), "ncclGroupEnd");
+  for (int q = 0; q < P; ++q)
+    cudaMemcpy2DAsync(dst[0] + q * w, dpitch, rb + q * chunk, w, w, nzl, cudaMemcpyDeviceToDevice, st);
+  return ok;
+#else
+  return false;
+#endif
+}
+
+// In-place all-reduce of `count` doubles at ptr[s] (per local slab).
+bool comm_allreduce(topt_ctx* c, const std::vector<double*>& ptr, int count, bool is_max, cudaStream_t st) {
+  const Comm& cm = c->comm;
+  if (cm.P == 1 || count <= 0) return true;
+  if (cm.emulated()) {
+    PtrList L{};
+    for (int s = 0; s < cm.P && s < 64; ++s) L.p[s] = ptr[s];
+    k_allreduce_emul<<<1, 64, 0, st>>>(L, cm.P, count, is_max ? 1 : 0);
+    count_launch();
+    return cudaGetLastError() == cudaSuccess;
+  }
+#ifdef TOPT_WITH_NCCL
+  return nccl_ok(ncclAllReduce(ptr[0], ptr[0], count, ncclDouble, is_max ? ncclMax : ncclSum, cm.nccl, st),
+                 "ncclAllReduce");
+#else
+  return false;
+#endif
+}
+
+}  // namespace topt

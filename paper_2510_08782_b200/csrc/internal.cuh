@@ -21,6 +21,12 @@ struct Geom {
   int lx, ly, lz;   // log2 of extents
   size_t F;         // points per scalar field
   float cx, cy, cz; // dt / h_a  (cells per unit velocity per time step)
+  // z-slab decomposition (world > 1).  zh > 0: interpolated INPUT fields carry zh halo planes
+  // on each side ([zh + nz + zh] planes, pointer = first halo plane) and z is not wrapped.
+  int zh;
+  // y-slab geometry of the z passes: global y offset of local row 0 and global ny (0 = local)
+  int ky0, nyg;
+  int* haloerr;     // device flag: set to 1 when a foot leaves the halo (zh > 0)
 };
 
 // Reduction helper: per-block fp64 partials, finalised in fixed order.
@@ -82,10 +88,24 @@ void launch_vchain(const Geom& g, const float* v, double2* Zv, float* u, double 
                    cudaStream_t st);
 // b-chain up to the x^-1 pass (Zb = 4 float2 fields of F); see kernels_spectral.cu
 void launch_bchain(const Geom& g, const float* b, float2* Zb, double alpha, int p, bool leray, cudaStream_t st);
+// chain phases (z-slab decomposition runs the last-axis pass on a y-slab geometry)
+int vchain_nin(const Geom& g, bool leray);
+int vchain_nout(const Geom& g);
+int bchain_nin(const Geom& g, bool leray);
+int bchain_nout(const Geom& g, bool leray);
+void vchain_xy(const Geom& g, const float* v, double2* const* Z, bool leray, cudaStream_t st);
+void vchain_last(const Geom& gz, double2* const* Z, double alpha, int p, bool leray, double n_total,
+                 cudaStream_t st);
+void vchain_inv(const Geom& g, double2* const* Z, float* u, cudaStream_t st);
+void bchain_xy(const Geom& g, const float* b, float2* const* Z, bool leray, cudaStream_t st);
+void bchain_last(const Geom& gz, float2* const* Z, double alpha, int p, bool leray, double n_total,
+                 cudaStream_t st);
+void bchain_yinv(const Geom& g, float2* const* Z, bool leray, cudaStream_t st);
 // x^-1 of the b-chain and pointwise assembly g = u + b_L, s = -(v - vbar) + p, with
 // partial sums in slots 0..9 (max|g|, sum gs, sum vu, sum su, sum g_c (3), sum s_c (3)).
 void launch_assemble(const Geom& g, const float2* Zb, bool leray, const float* b, const float* u, const float* v,
-                     const double* vsum, float* gout, float* sout, double* partials, int* nparts, cudaStream_t st);
+                     const double* vsum, float* gout, float* sout, double* partials, int* nparts, cudaStream_t st,
+                     double ntot = 0.0);
 
 // Internal scalars (per evaluation, device): sums used to finish the public scalars.
 enum { I_SUMV = 0, I_GMAX = 3, I_GS = 4, I_VU = 5, I_SU = 6, I_SUMG = 7, I_SUMS = 10, I_COUNT = 16 };

@@ -58,13 +58,17 @@ __device__ __forceinline__ float gather_global(const Geom& g, const float* __res
                                                float dx, float dy, float dz) {
   const float fx = floorf(dx), fy = floorf(dy), fz = floorf(dz);
   const int ix = x + (int)fx, iy = y + (int)fy, iz = z + (int)fz;
+  if (g.zh && (iz - 1 < -g.zh || iz + 2 >= g.nz + g.zh)) {  // foot beyond the neighbour's halo
+    if (g.haloerr) *g.haloerr = 1;
+    return 0.0f;
+  }
   float wx[4], wy[4], wz[4];
   lag4(dx - fx, wx);
   lag4(dy - fy, wy);
   lag4(dz - fz, wz);
   float acc = 0.0f;
   for (int c = 0; c < 4; ++c) {
-    const size_t zb = (size_t)((iz - 1 + c) & (g.nz - 1)) * g.ny;
+    const size_t zb = (size_t)(g.zh ? iz - 1 + c + g.zh : ((iz - 1 + c) & (g.nz - 1))) * g.ny;
     float rc = 0.0f;
     for (int b = 0; b < 4; ++b) {
       const float* row = f + (zb + ((iy - 1 + b) & (g.ny - 1))) * g.nx;
@@ -98,12 +102,14 @@ __global__ void __launch_bounds__(256) k_sl_tiled(Geom g, int ZC, TileArgs a) {
   const bool loader = threadIdx.x < NLOAD;
   const int ld_r = threadIdx.x / (XW / 4), ld_k = threadIdx.x % (XW / 4);
   const size_t ld_off = (size_t)((y0 - HALO + ld_r) & (g.ny - 1)) * g.nx + ((x0 - XH + 4 * ld_k) & (g.nx - 1));
+  // input plane p (slab-local, may be negative / past nz): periodic wrap, or the halo'd slab buffer
+  auto pin = [&](int p) -> size_t { return (size_t)(g.zh ? p + g.zh : (p & (g.nz - 1))) * plane; };
   const int ld_s = ld_r * PW + 4 * ld_k;
 
 #pragma unroll 1
   for (int s = 0; s < 2 * HALO + 1; ++s) {
     if (loader) {
-      const size_t po = (size_t)((z0 - HALO + s) & (g.nz - 1)) * plane + ld_off;
+      const size_t po = pin(z0 - HALO + s) + ld_off;
 #pragma unroll
       for (int f = 0; f < NF; ++f)
         *reinterpret_cast<float4*>(sm + (f * NZR + s) * PS + ld_s) = __ldg(reinterpret_cast<const float4*>(a.in[f] + po));
@@ -126,7 +132,7 @@ __global__ void __launch_bounds__(256) k_sl_tiled(Geom g, int ZC, TileArgs a) {
     float4 pre[NF];
     const bool pf = loader && (zi + 1 < ZC);
     if (pf) {
-      const size_t po = (size_t)((z + HALO + 1) & (g.nz - 1)) * plane + ld_off;
+      const size_t po = pin(z + HALO + 1) + ld_off;
 #pragma unroll
       for (int f = 0; f < NF; ++f) pre[f] = __ldg(reinterpret_cast<const float4*>(a.in[f] + po));
     }
@@ -257,10 +263,15 @@ __global__ void __launch_bounds__(256) k_sl_tiled(Geom g, int ZC, TileArgs a) {
 }
 
 bool tiled_ok(const Geom& g) {
-  return g.d == 3 && g.nx >= tiled::TX && g.nx % tiled::TX == 0 && g.ny % tiled::TY == 0 && g.nz >= 8;
+  return g.d == 3 && g.nx >= tiled::TX && g.nx % tiled::TX == 0 && g.ny % tiled::TY == 0 &&
+         (g.zh ? g.nz >= 1 : g.nz >= 8);
 }
 
-static int tiled_zc(const Geom& g) { return g.nz < 64 ? g.nz : 64; }
+static int tiled_zc(const Geom& g) {
+  int zc = g.nz < 64 ? g.nz : 64;
+  while (g.nz % zc) zc >>= 1;
+  return zc;
+}
 
 int tiled_blocks(const Geom& g) { return (g.nx / tiled::TX) * (g.ny / tiled::TY) * (g.nz / tiled_zc(g)); }
 

@@ -472,8 +472,9 @@ __global__ void __launch_bounds__(kThreads) k_pstrided(Geom g, int axis, int TXC
         const double kx = qx <= g.nx / 2 ? qx : qx - g.nx, kxp = qx == g.nx / 2 ? 0.0 : kx;
         double ky, kyp, kz, kzp;
         if (g.d == 3) {
-          const int qy = outer;
-          ky = qy <= g.ny / 2 ? qy : qy - g.ny; kyp = qy == g.ny / 2 ? 0.0 : ky;
+          const int nyg = g.nyg ? g.nyg : g.ny;  // y-slab layout: global row = ky0 + local row
+          const int qy = outer + g.ky0;
+          ky = qy <= nyg / 2 ? qy : qy - nyg; kyp = qy == nyg / 2 ? 0.0 : ky;
           kz = q <= N / 2 ? q : q - N; kzp = q == N / 2 ? 0.0 : kz;
         } else {
           ky = q <= N / 2 ? q : q - N; kyp = q == N / 2 ? 0.0 : ky;
@@ -553,6 +554,7 @@ struct AsmArgs {
   float* g;            // d*F or null
   float* s;            // d*F or null
   double* partials;    // [10][kMaxPartials]
+  double ntot;         // global point count (vbar = vsum / ntot)
 };
 
 template <int N>
@@ -576,7 +578,7 @@ __global__ void __launch_bounds__(kThreads) k_assemble(Geom g, int RB, int lpr, 
   const int myline = threadIdx.x / L::T, tid = threadIdx.x % L::T;
   fft_line<N, true>(buf + myline * L::STRIDE, tw, tid, myline < nlines);
   double gmax = 0.0, sgs = 0.0, svu = 0.0, ssu = 0.0, sg[3] = {0, 0, 0}, ss[3] = {0, 0, 0};
-  const double nF = (double)g.F;
+  const double nF = a.ntot;
   const int pf = leray ? lpr / 2 : 0;  // first p field
   for (int i4 = threadIdx.x; i4 < RB * N / 4; i4 += blockDim.x) {
     const int r = (4 * i4) / N, x = (4 * i4) % N;
@@ -703,64 +705,108 @@ static void pstrided_launch(const Geom& g, int axis, const ZList<C>& Z, int nin,
     default: fprintf(stderr, "topt: unsupported N %d\n", NV);       \
   }
 
-// u = alpha L v (P_L first if leray) with fp64 arithmetic and fp64 intermediates.
-// Zv: 3 double2 fields of F.
-void launch_vchain(const Geom& g, const float* v, double2* Zv, float* u, double alpha, int p, bool leray,
-                   cudaStream_t st) {
+// ---- chain phases (the z pass may run on a y-slab geometry between two transposes) ----------
+// v-chain: u = alpha L v (P_L first if leray), fp64 arithmetic and intermediates.
+// Fields: leray ? d real inputs (v_c + i 0) : (v_x + i v_y)[, (v_z)]; outputs (u_x + i u_y)[, (u_z)].
+int vchain_nin(const Geom& g, bool leray) { return leray ? g.d : (g.d == 3 ? 2 : 1); }
+int vchain_nout(const Geom& g) { return g.d == 3 ? 2 : 1; }
+int bchain_nin(const Geom& g, bool leray) { return leray ? g.d : (g.d == 3 ? 2 : 1); }
+int bchain_nout(const Geom& g, bool leray) { return leray ? (g.d == 3 ? 4 : 2) : (g.d == 3 ? 2 : 1); }
+
+void vchain_xy(const Geom& g, const float* v, double2* const* Z, bool leray, cudaStream_t st) {
   const size_t F = g.F;
-  ZList<double2> Z{{Zv, Zv + F, Zv + 2 * F, nullptr}};
-  SpecOp op{alpha, p, 1.0 / (double)F};
+  ZList<double2> L{{Z[0], Z[1], Z[2], nullptr}};
   RealIn in{};
-  int nin, nout = g.d == 3 ? 2 : 1;
+  const int nin = vchain_nin(g, leray);
   if (leray) {
-    nin = g.d;
     for (int c = 0; c < g.d; ++c) { in.re[c] = v + c * F; in.im[c] = nullptr; }
   } else {
-    nin = nout;
     in.re[0] = v; in.im[0] = v + F;
     if (g.d == 3) { in.re[1] = v + 2 * F; in.im[1] = nullptr; }
   }
-  const int last_axis = g.d == 3 ? 2 : 1;
-  const int Nl = g.d == 3 ? g.nz : g.ny;
-  TOPT_DISPATCH_N2(g.nx, (px_fwd_launch<N_, double2>(g, in, Z, nin, st)));
-  if (g.d == 3) TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 0, double2>(g, 1, Z, nin, nin, op, st)));
-  if (leray) {
-    TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 5, double2>(g, last_axis, Z, nin, nout, op, st)));
-  } else {
-    TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 2, double2>(g, last_axis, Z, nin, nout, op, st)));
-  }
-  if (g.d == 3) TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 1, double2>(g, 1, Z, nout, nout, op, st)));
-  RealOut out{{u, g.d == 3 ? u + 2 * F : nullptr, nullptr}, {u + F, nullptr, nullptr}};
-  TOPT_DISPATCH_N2(g.nx, (px_inv_launch<N_, double2>(g, Z, out, nout, st)));
+  SpecOp op{0.0, 1, 1.0};
+  TOPT_DISPATCH_N2(g.nx, (px_fwd_launch<N_, double2>(g, in, L, nin, st)));
+  if (g.d == 3) TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 0, double2>(g, 1, L, nin, nin, op, st)));
 }
 
-// b-chain up to (not including) the x^-1 pass, which the assembly kernel performs.
-// Zb: 4 float2 fields of F.
-void launch_bchain(const Geom& g, const float* b, float2* Zb, double alpha, int p, bool leray, cudaStream_t st) {
-  const size_t F = g.F;
-  SpecOp op{alpha, p, 1.0 / (double)F};
-  ZList<float2> Z{{Zb, Zb + F, Zb + 2 * F, Zb + 3 * F}};
-  int nin, nout;
-  RealIn in{};
+// z pass (3D) or y pass (2D) with the spectral operator, on geometry gz (z-slab when P == 1,
+// y-slab [nz][ny/P][nx] with ky0 / nyg set otherwise).  n_total = global point count.
+void vchain_last(const Geom& gz, double2* const* Z, double alpha, int p, bool leray, double n_total,
+                 cudaStream_t st) {
+  ZList<double2> L{{Z[0], Z[1], Z[2], nullptr}};
+  SpecOp op{alpha, p, 1.0 / n_total};
+  const int nin = vchain_nin(gz, leray), nout = vchain_nout(gz);
+  const int axis = gz.d == 3 ? 2 : 1, Nl = gz.d == 3 ? gz.nz : gz.ny;
   if (leray) {
-    nin = g.d;
-    nout = g.d == 3 ? 4 : 2;
+    TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 5, double2>(gz, axis, L, nin, nout, op, st)));
+  } else {
+    TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 2, double2>(gz, axis, L, nin, nout, op, st)));
+  }
+}
+
+void vchain_inv(const Geom& g, double2* const* Z, float* u, cudaStream_t st) {
+  const size_t F = g.F;
+  ZList<double2> L{{Z[0], Z[1], Z[2], nullptr}};
+  const int nout = vchain_nout(g);
+  SpecOp op{0.0, 1, 1.0};
+  if (g.d == 3) TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 1, double2>(g, 1, L, nout, nout, op, st)));
+  RealOut out{{u, g.d == 3 ? u + 2 * F : nullptr, nullptr}, {u + F, nullptr, nullptr}};
+  TOPT_DISPATCH_N2(g.nx, (px_inv_launch<N_, double2>(g, L, out, nout, st)));
+}
+
+// b-chain: x (and y) forward passes.
+void bchain_xy(const Geom& g, const float* b, float2* const* Z, bool leray, cudaStream_t st) {
+  const size_t F = g.F;
+  ZList<float2> L{{Z[0], Z[1], Z[2], Z[3]}};
+  RealIn in{};
+  const int nin = bchain_nin(g, leray);
+  if (leray) {
     for (int c = 0; c < g.d; ++c) { in.re[c] = b + c * F; in.im[c] = nullptr; }
   } else {
-    nin = nout = g.d == 3 ? 2 : 1;
     in.re[0] = b; in.im[0] = b + F;
     if (g.d == 3) { in.re[1] = b + 2 * F; in.im[1] = nullptr; }
   }
-  TOPT_DISPATCH_N2(g.nx, (px_fwd_launch<N_, float2>(g, in, Z, nin, st)));
-  const int last_axis = g.d == 3 ? 2 : 1;
-  const int Nl = g.d == 3 ? g.nz : g.ny;
-  if (g.d == 3) TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 0, float2>(g, 1, Z, nin, nin, op, st)));
+  SpecOp op{0.0, 1, 1.0};
+  TOPT_DISPATCH_N2(g.nx, (px_fwd_launch<N_, float2>(g, in, L, nin, st)));
+  if (g.d == 3) TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 0, float2>(g, 1, L, nin, nin, op, st)));
+}
+
+void bchain_last(const Geom& gz, float2* const* Z, double alpha, int p, bool leray, double n_total,
+                 cudaStream_t st) {
+  ZList<float2> L{{Z[0], Z[1], Z[2], Z[3]}};
+  SpecOp op{alpha, p, 1.0 / n_total};
+  const int nin = bchain_nin(gz, leray), nout = bchain_nout(gz, leray);
+  const int axis = gz.d == 3 ? 2 : 1, Nl = gz.d == 3 ? gz.nz : gz.ny;
   if (leray) {
-    TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 4, float2>(g, last_axis, Z, nin, nout, op, st)));
+    TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 4, float2>(gz, axis, L, nin, nout, op, st)));
   } else {
-    TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 3, float2>(g, last_axis, Z, nin, nout, op, st)));
+    TOPT_DISPATCH_N2(Nl, (pstrided_launch<N_, 3, float2>(gz, axis, L, nin, nout, op, st)));
   }
-  if (g.d == 3) TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 1, float2>(g, 1, Z, nout, nout, op, st)));
+}
+
+// y^-1 pass of the b-chain (3D); the x^-1 pass is fused into the assembly.
+void bchain_yinv(const Geom& g, float2* const* Z, bool leray, cudaStream_t st) {
+  if (g.d != 3) return;
+  ZList<float2> L{{Z[0], Z[1], Z[2], Z[3]}};
+  const int nout = bchain_nout(g, leray);
+  SpecOp op{0.0, 1, 1.0};
+  TOPT_DISPATCH_N2(g.ny, (pstrided_launch<N_, 1, float2>(g, 1, L, nout, nout, op, st)));
+}
+
+// single-slab compositions
+void launch_vchain(const Geom& g, const float* v, double2* Zv, float* u, double alpha, int p, bool leray,
+                   cudaStream_t st) {
+  double2* Z[3] = {Zv, Zv + g.F, Zv + 2 * g.F};
+  vchain_xy(g, v, Z, leray, st);
+  vchain_last(g, Z, alpha, p, leray, (double)g.F, st);
+  vchain_inv(g, Z, u, st);
+}
+
+void launch_bchain(const Geom& g, const float* b, float2* Zb, double alpha, int p, bool leray, cudaStream_t st) {
+  float2* Z[4] = {Zb, Zb + g.F, Zb + 2 * g.F, Zb + 3 * g.F};
+  bchain_xy(g, b, Z, leray, st);
+  bchain_last(g, Z, alpha, p, leray, (double)g.F, st);
+  bchain_yinv(g, Z, leray, st);
 }
 
 template <int N>
@@ -780,9 +826,10 @@ static void assemble_launch(const Geom& g, bool leray, const AsmArgs& a, int* np
 }
 
 void launch_assemble(const Geom& g, const float2* Zb, bool leray, const float* b, const float* u, const float* v,
-                     const double* vsum, float* gout, float* sout, double* partials, int* nparts, cudaStream_t st) {
+                     const double* vsum, float* gout, float* sout, double* partials, int* nparts, cudaStream_t st,
+                     double ntot) {
   const size_t F = g.F;
-  AsmArgs a{{Zb, Zb + F, Zb + 2 * F, Zb + 3 * F}, b, u, v, vsum, gout, sout, partials};
+  AsmArgs a{{Zb, Zb + F, Zb + 2 * F, Zb + 3 * F}, b, u, v, vsum, gout, sout, partials, ntot > 0 ? ntot : (double)F};
   TOPT_DISPATCH_N2(g.nx, (assemble_launch<N_>(g, leray, a, nparts, st)));
 }
 

@@ -37,12 +37,12 @@ def case(config, n, scale=0.5, model=None, nt=None, alpha=None, reg_order=None):
     return d
 
 
-def topt_for(d, **kw):
+def topt_for(d, world=1, **kw):
     import paper_2510_08782_b200 as topt
     cfg = topt.Config(n=tuple(d["n"]), nt=d["nt"], model=d["model"], reg_order=d["reg_order"],
                       alpha=d["alpha"], window=kw.pop("window", d.get("window", 5)),
                       sigma=kw.pop("sigma", d.get("sigma", 1)), tau=kw.pop("tau", d.get("tau", 0)), **kw)
-    return topt.Topt(cfg, device="cuda:0")
+    return topt.Topt(cfg, device="cuda:0", world=world)
 
 
 def dev(x):

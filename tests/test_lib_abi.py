@@ -41,8 +41,17 @@ def test_param_validation_without_gpu():
         assert LIB.topt_create(ctypes.byref(p), 0, 1, None, 0, ctypes.byref(ctx)) == -1
     p = Config(n=(96, 64), nt=4).params()   # even but not a power of two
     assert LIB.topt_create(ctypes.byref(p), 0, 1, None, 0, ctypes.byref(ctx)) == -2
+    # z-slab decomposition parameter checks (world > 1)
     p = Config(n=(64, 64, 64), nt=4).params()
-    assert LIB.topt_create(ctypes.byref(p), 0, 2, None, 0, ctypes.byref(ctx)) in (-2, -4)
+    assert LIB.topt_create(ctypes.byref(p), 0, 3, None, 0, ctypes.byref(ctx)) == -1      # world not 2^k
+    p = Config(n=(64, 64, 16), nt=4).params()
+    assert LIB.topt_create(ctypes.byref(p), 0, 8, None, 0, ctypes.byref(ctx)) == -1      # nz/P < halo 4
+    p = Config(n=(64, 64), nt=4).params()
+    assert LIB.topt_create(ctypes.byref(p), 0, 2, None, 0, ctypes.byref(ctx)) == -1      # 2D on 2 ranks
+    p = Config(n=(16, 64, 64), nt=4).params()
+    assert LIB.topt_create(ctypes.byref(p), 0, 2, None, 0, ctypes.byref(ctx)) == -2      # nx < 32 tiles
+    p = Config(n=(64, 64, 64), nt=4).params()
+    assert LIB.topt_create(ctypes.byref(p), 1, 2, None, 0, ctypes.byref(ctx)) == -1      # emulation runs as rank 0
     assert b"" != LIB.topt_last_error()
 
 
