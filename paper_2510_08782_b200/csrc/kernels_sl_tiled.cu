@@ -288,7 +288,9 @@ void tiled_trace(const Geom& g, const float* v, float* df, float* da, double* vs
   TileArgs a{};
   a.partials = vsum;
   if (nparts) *nparts = tiled_blocks(g);
-  for (int c = 0; c < 3; ++c) a.in[c] = v + c * g.F;
+  // component stride of v: F, or F plus 2 zh halo planes for a halo'd slab copy
+  const size_t cs = g.F + 2 * (size_t)g.zh * g.nx * g.ny;
+  for (int c = 0; c < 3; ++c) a.in[c] = v + c * cs;
   a.out[0] = df;
   a.out[1] = da;
   launch_tiled<M_TRACE, 3, false, 2>(g, a, st);  // midpoint displacement dt/2 v: |floor| <= 1
