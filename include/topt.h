@@ -122,10 +122,18 @@ const char* topt_last_error(void);
  * topt_create on every rank.  Returns TOPT_ERR_UNSUPPORTED if built without NCCL. */
 topt_status topt_get_unique_id(uint8_t id[128]);
 
-/* Create a context for problem `p` on CUDA device `device`.  world >= 1 ranks split
- * the grid into z-slabs; n[2] % world must be 0.  `id` may be NULL
- * when world == 1.  Validates p (TOPT_ERR_INVALID_ARG: odd/small n, alpha <= 0,
- * sigma < 1, tau < 0, window < 0, dim not in {2,3}, nt < 1). */
+/* Create a context for problem `p` on CUDA device `device`.  world >= 1 (a power of two)
+ * splits the 3D grid into z-slabs of n[2]/world planes (BASELINE north_star):
+ *  - id != NULL: NCCL mode, one slab per process (`rank`); fields passed to every call are
+ *    this rank's slab [n[2]/world][n[1]][n[0]];
+ *  - id == NULL, world > 1: all slabs emulated in this process on `device` (exchanges are
+ *    device copies; rank must be 0); fields are whole-grid arrays.  Used to test that the
+ *    decomposition reproduces world == 1.
+ * Requires for world > 1: dim 3, n[1] and n[2] divisible by world, n[2]/world >= 4 (one
+ * neighbour's 4 halo planes), n[0] >= 32, n[1] % 8 == 0.  Validates p
+ * (TOPT_ERR_INVALID_ARG: odd/small n, alpha <= 0, sigma < 1, tau < 0, window < 0,
+ * dim not in {2,3}, nt < 1, bad world).  Per-operator entry points (feet, forward,
+ * get_adjoint, derivative, apply_precond, leray) need world == 1. */
 topt_status topt_create(const topt_params* p, int32_t rank, int32_t world, const uint8_t* id,
                         int32_t device, topt_ctx** out);
 
@@ -146,7 +154,10 @@ topt_status topt_local_slab(const topt_ctx* ctx, int32_t* z0, int32_t* nz);
 
 /* GA-NGMRES(w; sigma, tau) (Alg. 3) or GA-AA from v^0 = v_inout (the
  * paper uses v^0 = 0).  m0, m1: F each; v_inout: d*F, overwritten with the
- * final iterate.  Synchronous (host decisions: Armijo, LSQ); report filled on exit. */
+ * final iterate.  Synchronous (host decisions: Armijo, LSQ); report filled on exit.
+ * z-slabs (world > 1): an Armijo trial whose characteristic foot leaves the 4-plane halo
+ * (|delta_z| > 3 cells) is rejected like a failed Armijo test; an accepted iterate whose
+ * foot does returns TOPT_ERR_HALO. */
 topt_status topt_solve(topt_ctx* ctx, const float* m0, const float* m1, float* v_inout,
                        topt_report* report, void* stream);
 

@@ -1256,7 +1256,13 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
         TOPT_CHECK_LAUNCH();
         ++obj_evals;
         HostScalars ts;
-        if ((r = fetch(c, 1, ts, st)) != TOPT_OK) return r;
+        r = fetch(c, 1, ts, st);
+        if (r == TOPT_ERR_HALO) {  // trial foot beyond the z-slab halo: reject the trial, backtrack
+          for (auto& sl : c->slabs) TOPT_CUDA(cudaMemsetAsync(sl.haloerr, 0, sizeof(int), st));
+          rho_t *= 0.5;
+          continue;
+        }
+        if (r != TOPT_OK) return r;
         // reg(v + rho s) = reg + rho alpha<s, L v> + rho^2/2 alpha<s, L s>  (exact: quadratic)
         const double reg_t = cur.pub(TOPT_S_REG) + rho_t * cur.pub(TOPT_S_SLV) +
                              0.5 * rho_t * rho_t * cur.pub(TOPT_S_SLS);
