@@ -9,9 +9,10 @@ force, alpha L v and the preconditioner), inputs resident in HBM.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl topt|reference]
 
-N > 1 (torchrun): every rank evaluates its own replica of the workload (weak scaling,
-no data-path collective; the z-slab path is not built yet — DESIGN.md §9); value =
-evaluations of all ranks / max-over-ranks device time.
+N > 1 (torchrun): the 256^3 grid is split into N z-slabs, one per GPU, exchanging halos,
+z<->y transposes and reductions over NCCL; value = evaluations of the one
+problem / max-over-ranks device time (strong scaling).  --parallel replica instead runs one
+independent replica per rank (weak scaling, no data-path collective).
 
 --impl reference: the fp64 CPU oracle (oracle/, test infrastructure) timed on the host
 cores on a bounded sample of the same workload, rank 0 only.
@@ -110,16 +111,52 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def _dist_init():
+def _dist_init(backend="nccl"):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     return rank, world, local
+
+
+def share_unique_id(rank, world, make_id):
+    """Rank 0 creates the 128-byte NCCL unique id; every rank receives it (torch.distributed)."""
+    import torch.distributed as dist
+    obj = [make_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def slab_planes(nz, rank, world):
+    """z-slab of `rank`: planes [z0, z0 + nz/world) (n[2] % world == 0)."""
+    nzl = nz // world
+    return rank * nzl, nzl
+
+
+def slab_of(field, rank, world, vector=False):
+    """This rank's z-slab of a whole-grid array (numpy [..., nz, ny, nx]), contiguous."""
+    import numpy as np
+    nz = field.shape[-3]
+    z0, nzl = slab_planes(nz, rank, world)
+    return np.ascontiguousarray(field[..., z0:z0 + nzl, :, :])
+
+
+def max_over_ranks(x, world, device=None):
+    """Max of a float over ranks (device time of the slowest rank)."""
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def _cpu_threads():
@@ -205,14 +242,22 @@ def run_topt(args):
     n = tuple(args.n) if args.n else None
     d = make_problem(args.config, n, device=str(dev))
     cfgp = dict(n=tuple(d["n"]), nt=d["nt"], model=d["model"], reg_order=d["reg_order"], alpha=d["alpha"])
-    t = topt.Topt(topt.Config(window=d["window"], **cfgp), device=dev)
-    m0 = torch.tensor(d["m0"], dtype=torch.float32, device=dev)
-    m1 = torch.tensor(d["m1"], dtype=torch.float32, device=dev)
-    v = torch.tensor(d["vstar"], dtype=torch.float32, device=dev)  # representative displacement
+    slab = world > 1 and args.parallel == "slab"
+    if slab:  # one z-slab per GPU over NCCL
+        uid = share_unique_id(rank, world, topt.get_unique_id)
+        t = topt.Topt(topt.Config(window=d["window"], **cfgp), device=dev, rank=rank, world=world, unique_id=uid)
+        m0n, m1n = slab_of(d["m0"], rank, world), slab_of(d["m1"], rank, world)
+        vn = slab_of(d["vstar"], rank, world, vector=True)
+    else:
+        t = topt.Topt(topt.Config(window=d["window"], **cfgp), device=dev)
+        m0n, m1n, vn = d["m0"], d["m1"], d["vstar"]
+    m0 = torch.tensor(m0n, dtype=torch.float32, device=dev)
+    m1 = torch.tensor(m1n, dtype=torch.float32, device=dev)
+    v = torch.tensor(vn, dtype=torch.float32, device=dev)  # representative displacement
     g = torch.empty_like(v)
     s = torch.empty_like(v)
     sc = torch.zeros(16, dtype=torch.float64, device=dev)
-    npts = int(np.prod(d["n"]))
+    npts = int(np.prod(m0n.shape))  # points of this rank
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -236,12 +281,10 @@ def run_topt(args):
         torch.cuda.synchronize()
         launches = topt.Topt.launch_count() - l0
         ms = e0.elapsed_time(e1)
-    if world > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms = float(tt.item())
+    ms = max_over_ranks(ms, world, dev)
     ms_per_step = ms / args.steps
-    value = world * args.steps / (ms / 1e3)
+    evals = args.steps if slab else world * args.steps  # slab: the ranks share one problem
+    value = evals / (ms / 1e3)
 
     # per-kernel-class breakdown, separate (un-timed) pass with event brackets
     t.profile(True)
@@ -272,14 +315,14 @@ def run_topt(args):
     breakdown = {x["name"]: {"share": round(x["ms"] / total_ms, 4),
                              "GB/s": round(x["bytes"] / (x["ms"] / 1e3) / 1e9, 1) if x["bytes"] else None,
                              "launches_per_step": x["launches"] / args.steps} for x in kern}
-    model_bytes = _pass_model_bytes(cfgp)
+    model_bytes = _pass_model_bytes(cfgp) / (world if slab else 1)  # per rank
 
     # end to end through the public API with HOST buffers (pinned): H2D m0, m1, v; D2H g + scalars
     e2e = None
     if not args.no_e2e:
-        m0h = torch.tensor(d["m0"], dtype=torch.float32).pin_memory()
-        m1h = torch.tensor(d["m1"], dtype=torch.float32).pin_memory()
-        vh = torch.tensor(d["vstar"], dtype=torch.float32).pin_memory()
+        m0h = torch.tensor(m0n, dtype=torch.float32).pin_memory()
+        m1h = torch.tensor(m1n, dtype=torch.float32).pin_memory()
+        vh = torch.tensor(vn, dtype=torch.float32).pin_memory()
         gh = torch.empty_like(vh).pin_memory()
         sch = torch.zeros(16, dtype=torch.float64).pin_memory()
         for _ in range(max(1, args.warmup)):
@@ -292,12 +335,8 @@ def run_topt(args):
             t.eval_gradient_host(m0h, m1h, vh, gh, sch)
         f1.record(stream)
         torch.cuda.synchronize()
-        ems = f0.elapsed_time(f1)
-        if world > 1:
-            tt = torch.tensor([ems], dtype=torch.float64, device=dev)
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            ems = float(tt.item())
-        e2e = {"value": world * args.steps / (ems / 1e3), "unit": UNIT,
+        ems = max_over_ranks(f0.elapsed_time(f1), world, dev)
+        e2e = {"value": evals / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(4 * npts * (2 + len(d["n"]))),
                "d2h_bytes_per_step": int(4 * npts * len(d["n"]) + 16 * 8)}
 
@@ -316,17 +355,17 @@ def run_topt(args):
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "strong" if slab else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": wl, "grid": list(d["n"]), "nt": d["nt"], "model": d["model"],
                        "reg_order": d["reg_order"], "alpha": d["alpha"],
-                       "parallelism": "replicas" if world > 1 else "single",
+                       "parallelism": (f"zslab{world}" if slab else f"replicas{world}") if world > 1 else "single",
                        "l2": "inputs larger than L2 (~15 GB of HBM traffic per evaluation vs 126 MB L2)"},
             "clocks": clk.summary(),
             "e2e": e2e,
             "gpu_launches": launches,
             "roofline": roofline,
             "cpu_baseline": cpu,
-            "hbm_frac_pass_model": round(model_bytes * value / (world * peak * 1e9), 4),
+            "hbm_frac_pass_model": round(model_bytes * (value if slab else value / world) / (peak * 1e9), 4),
             "pass_model_bytes_per_eval": model_bytes,
             "kernels": breakdown,
         }
@@ -346,6 +385,8 @@ def main():
     ap.add_argument("--cpu-n", type=int, default=128, help="oracle sample grid for cpu_baseline")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--parallel", default="slab", choices=["slab", "replica"],
+                    help="N > 1: z-slabs over NCCL (one problem) or independent replicas")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

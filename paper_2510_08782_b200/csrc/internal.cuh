@@ -117,6 +117,7 @@ void launch_finalize(const double* partials, int slot, int nparts, double scale,
 void launch_finalize_multi(const double* partials, int slot0, int nslots, int nparts, double scale,
                            double* dst, cudaStream_t st);
 void launch_combine_obj(double* scalars, cudaStream_t st);  // OBJ = DIST + REG
+void launch_flag_to_double(const int* f, double* d, cudaStream_t st);
 // finalize slots [first, first+count) (slot 0 of the assembly = max) into dst
 void launch_finalize_slots(const double* partials, int first, int count, int nparts, bool first_is_max,
                            double* dst, cudaStream_t st);

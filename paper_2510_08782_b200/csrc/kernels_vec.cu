@@ -89,6 +89,11 @@ void launch_finish(const double* isc, double* sc, int d, double n, double cellvo
   k_finish<<<1, 1, 0, st>>>(isc, sc, d, n, cellvol);
   count_launch();
 }
+__global__ void k_flag_to_double(const int* f, double* d) { *d = (double)*f; }
+void launch_flag_to_double(const int* f, double* d, cudaStream_t st) {
+  k_flag_to_double<<<1, 1, 0, st>>>(f, d);
+  count_launch();
+}
 void launch_combine_obj(double* scalars, cudaStream_t st) { k_combine_obj<<<1, 1, 0, st>>>(scalars);   count_launch();
 }
 
