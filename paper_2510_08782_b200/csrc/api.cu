@@ -203,6 +203,12 @@ topt_status topt_create(const topt_params* p, int32_t rank, int32_t world, const
   c->slab_bytes = b;
   c->ws_need = b * c->comm.nloc;
   upload_twiddles();
+  if (c->comm.P == 1) {  // side stream for v-only work (eval_gradient), see eval_gradient
+    cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_div, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_u, cudaEventDisableTiming);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     delete c;
@@ -216,6 +222,13 @@ topt_status topt_destroy(topt_ctx* ctx) {
   if (!ctx) return fail(TOPT_ERR_INVALID_ARG, "ctx is NULL");
   for (auto& r : ctx->recs) { ctx->pool.push_back(r.a); ctx->pool.push_back(r.b); }
   for (auto e : ctx->pool) cudaEventDestroy(e);
+  if (ctx->side) {
+    cudaStreamSynchronize(ctx->side);
+    cudaStreamDestroy(ctx->side);
+    cudaEventDestroy(ctx->ev_fork);
+    cudaEventDestroy(ctx->ev_div);
+    cudaEventDestroy(ctx->ev_u);
+  }
 #ifdef TOPT_WITH_NCCL
   if (ctx->comm.nccl) ncclCommDestroy(ctx->comm.nccl);
 #endif
@@ -430,6 +443,51 @@ void compute_div(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
   }
 }
 
+// u = alpha L v by the fp64 v-chain (P_L first for incompressible, R9) into utmp; io[].u := utmp
+void run_vchain(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
+  const int P = P_of(c);
+  const size_t F = c->F;
+  const double F4 = 4.0 * F, d = c->d;
+  const bool leray = c->p.model == TOPT_INCOMPRESSIBLE;
+  const double half = c->d == 3 ? 2.0 : 1.0;
+  const double n_all = ntot(c);
+  {
+    const double nin = leray ? d : half, nout = half, F16 = 16.0 * F;
+    const double bytes = d * F4 + nin * F16 + (c->d == 3 ? 2 * nin * F16 + 2 * nout * F16 : 0.0) +
+                         (nin + nout) * F16 + nout * F16 + d * F4;
+    Prof pr(c, K_VCHAIN, bytes * c->comm.nloc, c->d == 3 ? 5 : 3, st);
+    const int vin = vchain_nin(c->slabs[0].g, leray), vout = vchain_nout(c->slabs[0].g);
+    for (size_t si = 0; si < c->slabs.size(); ++si) {
+      Slab& sl = c->slabs[si];
+      double2* Z[3] = {sl.Zv, sl.Zv + F, sl.Zv + 2 * F};
+      vchain_xy(sl.g, io[si].v, Z, leray, st);
+    }
+    if (P > 1)
+      for (int f = 0; f < vin; ++f) {
+        std::vector<double2*> a, b;
+        for (auto& sl : c->slabs) { a.push_back(sl.Zv + f * F); b.push_back(sl.Zvy + f * F); }
+        tz2y(c, a, b, st);
+      }
+    for (auto& sl : c->slabs) {
+      double2* base = P > 1 ? sl.Zvy : sl.Zv;
+      double2* Z[3] = {base, base + F, base + 2 * F};
+      vchain_last(P > 1 ? sl.gy : sl.g, Z, c->p.alpha, c->p.reg_order, leray, n_all, st);
+    }
+    if (P > 1)
+      for (int f = 0; f < vout; ++f) {
+        std::vector<double2*> a, b;
+        for (auto& sl : c->slabs) { a.push_back(sl.Zvy + f * F); b.push_back(sl.Zv + f * F); }
+        ty2z(c, a, b, st);
+      }
+    for (size_t si = 0; si < c->slabs.size(); ++si) {
+      Slab& sl = c->slabs[si];
+      double2* Z[3] = {sl.Zv, sl.Zv + F, sl.Zv + 2 * F};
+      vchain_inv(sl.g, Z, sl.utmp, st);
+      io[si].u = sl.utmp;
+    }
+  }
+}
+
 // Forward half: feet (R6), static factor (continuity, R7), m^0..m^S, lam^S = m1 - m^S
 // (R1/R8), dist -> scal[DIST], sum_x v_c -> isc[I_SUMV..] (all-reduced).
 void forward_half(topt_ctx* c, std::vector<Io>& io, bool want_adj, cudaStream_t st) {
@@ -456,7 +514,10 @@ void forward_half(topt_ctx* c, std::vector<Io>& io, bool want_adj, cudaStream_t 
   comm_allreduce(c, intls(io, I_SUMV), c->d, false, st);
   const bool cont = c->p.model == TOPT_CONTINUITY;
   if (cont) {
-    {
+    if (c->div_pending) {
+      cudaStreamWaitEvent(st, c->ev_div, 0);
+      c->div_pending = false;
+    } else {
       Prof pr(c, K_DIV, (3.0 * d - 1.0) * F4, c->d, st);
       compute_div(c, io, st);
     }
@@ -504,7 +565,10 @@ void backward_half(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
   const double F4 = 4.0 * F, d = c->d;
   const bool adv = c->p.model == TOPT_ADVECTION;
   if (adv) {
-    {
+    if (c->div_pending) {
+      cudaStreamWaitEvent(st, c->ev_div, 0);
+      c->div_pending = false;
+    } else {
       Prof pr(c, K_DIV, (3.0 * d - 1.0) * F4, c->d, st);
       compute_div(c, io, st);
     }
@@ -561,42 +625,13 @@ void backward_half(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
   const bool leray = c->p.model == TOPT_INCOMPRESSIBLE;
   const double half = c->d == 3 ? 2.0 : 1.0;
   const double n_all = ntot(c);
-  // v-chain: u = alpha L v (fp64) when not supplied
-  const bool need_u = io[0].u == nullptr;
-  if (need_u) {
-    const double nin = leray ? d : half, nout = half, F16 = 16.0 * F;
-    const double bytes = d * F4 + nin * F16 + (c->d == 3 ? 2 * nin * F16 + 2 * nout * F16 : 0.0) +
-                         (nin + nout) * F16 + nout * F16 + d * F4;
-    Prof pr(c, K_VCHAIN, bytes * c->comm.nloc, c->d == 3 ? 5 : 3, st);
-    const int vin = vchain_nin(c->slabs[0].g, leray), vout = vchain_nout(c->slabs[0].g);
-    for (size_t si = 0; si < c->slabs.size(); ++si) {
-      Slab& sl = c->slabs[si];
-      double2* Z[3] = {sl.Zv, sl.Zv + F, sl.Zv + 2 * F};
-      vchain_xy(sl.g, io[si].v, Z, leray, st);
-    }
-    if (P > 1)
-      for (int f = 0; f < vin; ++f) {
-        std::vector<double2*> a, b;
-        for (auto& sl : c->slabs) { a.push_back(sl.Zv + f * F); b.push_back(sl.Zvy + f * F); }
-        tz2y(c, a, b, st);
-      }
-    for (auto& sl : c->slabs) {
-      double2* base = P > 1 ? sl.Zvy : sl.Zv;
-      double2* Z[3] = {base, base + F, base + 2 * F};
-      vchain_last(P > 1 ? sl.gy : sl.g, Z, c->p.alpha, c->p.reg_order, leray, n_all, st);
-    }
-    if (P > 1)
-      for (int f = 0; f < vout; ++f) {
-        std::vector<double2*> a, b;
-        for (auto& sl : c->slabs) { a.push_back(sl.Zvy + f * F); b.push_back(sl.Zv + f * F); }
-        ty2z(c, a, b, st);
-      }
-    for (size_t si = 0; si < c->slabs.size(); ++si) {
-      Slab& sl = c->slabs[si];
-      double2* Z[3] = {sl.Zv, sl.Zv + F, sl.Zv + 2 * F};
-      vchain_inv(sl.g, Z, sl.utmp, st);
-      io[si].u = sl.utmp;
-    }
+  // v-chain: u = alpha L v (fp64) when not supplied (or already running on the side stream)
+  if (c->u_pending) {
+    cudaStreamWaitEvent(st, c->ev_u, 0);
+    c->u_pending = false;
+    for (size_t si = 0; si < c->slabs.size(); ++si) io[si].u = c->slabs[si].utmp;
+  } else if (io[0].u == nullptr) {
+    run_vchain(c, io, st);
   }
   {
     const double nin = leray ? d : half, nout = leray ? 2 * half : half, F8 = 8.0 * F;
@@ -647,7 +682,29 @@ void backward_half(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
   for (size_t si = 0; si < c->slabs.size(); ++si) launch_finish(io[si].isc, io[si].scal, c->d, n_all, c->cellvol, st);
 }
 
+// One objective + gradient evaluation.  On a single slab, div v and the fp64 v-chain
+// depend on v alone: they run on the library's side stream (forked from and joined back
+// into `st` by events) concurrently with the trace and the SL sweeps, which are bound by
+// shared memory and leave most of the HBM bandwidth idle.  With z-slabs (NCCL exchanges
+// inside both) everything stays on `st`.
 topt_status eval_gradient(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
+  c->div_pending = c->u_pending = false;
+  if (P_of(c) == 1 && c->side && io[0].u == nullptr) {
+    cudaEventRecord(c->ev_fork, st);
+    cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+    if (c->p.model != TOPT_INCOMPRESSIBLE) {
+      {
+        Prof pr(c, K_DIV, (3.0 * c->d - 1.0) * 4.0 * c->F, c->d, c->side);
+        compute_div(c, io, c->side);
+      }
+      cudaEventRecord(c->ev_div, c->side);
+      c->div_pending = true;
+    }
+    run_vchain(c, io, c->side);
+    for (auto& x : io) x.u = nullptr;  // set again when the v-chain is joined
+    cudaEventRecord(c->ev_u, c->side);
+    c->u_pending = true;
+  }
   forward_half(c, io, true, st);
   backward_half(c, io, st);
   TOPT_CHECK_LAUNCH();

@@ -76,6 +76,10 @@ struct topt_ctx {
   topt::Comm comm;
   std::vector<topt::Slab> slabs;
   std::vector<double> replay;
+  // side stream for work that depends on v only (eval_gradient, single slab)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_div = nullptr, ev_u = nullptr;
+  bool div_pending = false, u_pending = false;
   // per-kernel-class timing (topt_profile / topt_kernel_stats)
   bool prof = false;
   struct Rec { int cls; cudaEvent_t a, b; double bytes; int launches; };

@@ -2,33 +2,38 @@
 //
 // Same arithmetic as kernels_sl.cu (readings R5-R7): out(l) =
 // I[in](l + delta(l)) with the periodic tricubic Lagrange stencil, but the 64 taps are
-// gathered from shared memory instead of L1:
-//   * a block owns an output tile of 32 (x) x 8 (y) columns and marches through ZC planes
-//     in z; the input planes z-4 .. z+4 (tile + halo 4 in x and y) live in a ring of 10
-//     shared-memory slots; plane z+5 is prefetched into registers while plane z is
-//     computed (one float4 per loader thread, coalesced, periodic wrap in x/y/z);
-//   * one thread per output point per plane: a warp is one 128-byte x row of outputs, so the
-//     delta / E / output streams stay fully coalesced;
-//   * feet whose floor offsets leave [-3, 2] in any axis (|delta| > ~3 cells) fall back to
-//     the L1 gather of kernels_sl.cu for that point (correct for any CFL).
-// Smem rows are padded to a 64-word pitch (bank-conflict-free when a warp straddles rows or
-// planes).  Global traffic per output point ~ 1.6 input floats (halo) + the streams.
+// gathered from shared memory instead of L1.  A block owns an output tile of 32 (x) x 8 (y)
+// columns and marches through a chunk of z planes; the input planes around the current
+// plane (tile + halo 4 in x, H in y/z) live in a ring of shared-memory slots.  One thread
+// per output point per plane: a warp is one 128-byte x row of outputs, so the delta / E /
+// output streams stay fully coalesced; smem rows have a 64-word pitch, so lanes of a warp
+// that straddle two rows / planes hit disjoint banks.  Feet whose floor offsets leave the
+// halo fall back to the L1 gather for that point (correct for any CFL).
+//
+// Single-field kernels (SL step, last step, Heun factor): k_sl_pipe, a cp.async pipeline.
+//   * the ring has NZR = 2H + 2K = 16 slots (slot = plane & 15); the K planes of stage i+2
+//     are copied global -> shared with cp.async (no register staging, no loader role)
+//     while stage i is computed, so HBM latency is covered by 2 stages of K planes;
+//   * per stage: one wait + barrier before the K planes are computed, one barrier before
+//     their oldest slots are refilled — 2 barriers per K = 4 planes;
+//   * the per-point streams (delta, E) are prefetched into registers one plane ahead.
+// Trace (3 fields, RK2 midpoint feet): k_sl_trace, ring of 2H+2 slots with one plane
+// prefetched into registers (H = 2: the midpoint displacement dt/2 v has |floor| <= 1).
+#include <cmath>
+
 #include "internal.cuh"
 
 namespace topt {
 
 namespace tiled {
 constexpr int TX = 32, TY = 8;
-constexpr int XH = 4;                 // x halo (float4 aligned): foot floors in [-3, 2]
-constexpr int XW = TX + 2 * XH;       // 40 floats loaded per row
-constexpr int PW = 64;                // smem row pitch: a multiple of 32 words, so lanes of a warp that
-                                      // straddle two rows / planes hit disjoint banks
-template <int H>                      // y/z halo: foot floors in [-H+1, H-2]
+constexpr int XH = 4;            // x halo (float4 aligned): foot floors in [-3, 2]
+constexpr int XW = TX + 2 * XH;  // 40 floats loaded per row
+constexpr int PW = 64;           // smem row pitch: a multiple of 32 words
+template <int H>                 // y/z halo: foot floors in [-H+1, H-2]
 struct Cfg {
-  static constexpr int PH = TY + 2 * H;       // rows per plane
-  static constexpr int PS = PW * PH;          // floats per plane (multiple of 32)
-  static constexpr int NZR = 2 * H + 2;       // ring slots (planes z-H .. z+H + one prefetch)
-  static constexpr int NLOAD = (XW / 4) * PH; // float4 loads per plane
+  static constexpr int PH = TY + 2 * H;  // rows per plane
+  static constexpr int PS = PW * PH;     // floats per plane (multiple of 32)
 };
 }  // namespace tiled
 
@@ -41,16 +46,21 @@ struct TileArgs {
   const float* m1;      // LAST
   float* out[2];        // STEP/LAST/EFACTOR: out[0]; TRACE: out[0] = delta_f, out[1] = delta_a (3F each)
   float* lamS;          // LAST (may be null)
-  double* partials;     // LAST
+  double* partials;     // LAST / TRACE
   float sh, h2;         // EFACTOR: E = 1 + sh (a + b) + h2 a b
 };
 
+// Cubic Lagrange weights on nodes -1, 0, 1, 2 (R5) in 8 operations: with a = t (t - 1),
+// w0 = a (2 - t)/6, w1 = (t - 1)(a - 2)/2, w2 = -t (a - 2)/2, w3 = a (t + 1)/6.
+// t = 0 gives exactly (0, 1, 0, 0) (v = 0 is a bitwise identity).
 __device__ __forceinline__ void lag4(float t, float w[4]) {
-  const float tm1 = t - 1.0f, tm2 = t - 2.0f, tp1 = t + 1.0f;
-  w[0] = -t * tm1 * tm2 * (1.0f / 6.0f);
-  w[1] = tp1 * tm1 * tm2 * 0.5f;
-  w[2] = -tp1 * t * tm2 * 0.5f;
-  w[3] = tp1 * t * tm1 * (1.0f / 6.0f);
+  const float a = fmaf(t, t, -t);
+  const float c6 = a * (1.0f / 6.0f), c3 = a * (1.0f / 3.0f);
+  const float h = fmaf(a, 0.5f, -1.0f);
+  w[0] = fmaf(-t, c6, c3);
+  w[1] = fmaf(t, h, -h);
+  w[2] = -t * h;
+  w[3] = fmaf(t, c6, c6);
 }
 
 // Global-memory (L1) gather, periodic; fallback for feet outside the halo.
@@ -81,10 +91,201 @@ __device__ __forceinline__ float gather_global(const Geom& g, const float* __res
   return acc;
 }
 
-template <int MODE, int NF, bool HAS_E, int HALO>
-__global__ void __launch_bounds__(256) k_sl_tiled(Geom g, int ZC, TileArgs a) {
+// 64-tap tricubic gather of NF fields from smem planes (field stride FS floats); slot(c) =
+// smem offset of plane c (c = 0..3: planes iz-1 .. iz+2), rowoff = offset of the first tap.
+// Planes are taken in pairs (c, c+1) by packed fp32x2 FMAs with the x-y weight product
+// (one FMUL2 per tap, shared by both pairs): acc_{01} = sum_ab wx_a wy_b (f_{ab,0}, f_{ab,1}),
+// then the z weights (4 FMAs).
+template <int NF, int FS, typename SlotF>
+__device__ __forceinline__ void gather_smem(const float* sm, SlotF slot, int rowoff, const float wx[4],
+                                            const float wy[4], const float wz[4], float* res) {
+  using tiled::PW;
+  float2 wx2[4], wy2[4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    wx2[a] = make_float2(wx[a], wx[a]);
+    wy2[a] = make_float2(wy[a], wy[a]);
+  }
+  const int p0 = slot(0) + rowoff, p1 = slot(1) + rowoff, p2 = slot(2) + rowoff, p3 = slot(3) + rowoff;
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    const float* s0 = sm + f * FS;
+    float2 lo = make_float2(0.f, 0.f), hi = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int o = b * PW + a;
+        const float2 w = __fmul2_rn(wx2[a], wy2[b]);
+        lo = (a | b) ? __ffma2_rn(w, make_float2(s0[p0 + o], s0[p1 + o]), lo)
+                     : __fmul2_rn(w, make_float2(s0[p0 + o], s0[p1 + o]));
+        hi = (a | b) ? __ffma2_rn(w, make_float2(s0[p2 + o], s0[p3 + o]), hi)
+                     : __fmul2_rn(w, make_float2(s0[p2 + o], s0[p3 + o]));
+      }
+    res[f] = fmaf(wz[3], hi.y, fmaf(wz[2], hi.x, fmaf(wz[1], lo.y, wz[0] * lo.x)));
+  }
+}
+
+__device__ __forceinline__ void cp_async16(float* smem, const float* g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// =====================================================================================
+// Single-field pipelined kernel (STEP / LAST / EFACTOR).
+// =====================================================================================
+namespace pipe {
+constexpr int H = 4, K = 4;         // y/z halo; planes per pipeline stage
+constexpr int NZR = 2 * H + 2 * K;  // 16 ring slots (power of two)
+constexpr int PS = tiled::Cfg<H>::PS, PH = tiled::Cfg<H>::PH;
+constexpr int NF4 = PH * (tiled::XW / 4);  // float4 per plane
+constexpr size_t SMEM = (size_t)NZR * PS * sizeof(float);
+}  // namespace pipe
+
+#ifndef TOPT_SL_MINB
+#define TOPT_SL_MINB 3  // resident blocks per SM the register budget is sized for
+#endif
+template <int MODE, bool HAS_E>
+__global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, TileArgs a) {
   using namespace tiled;
-  constexpr int PS = Cfg<HALO>::PS, NZR = Cfg<HALO>::NZR, NLOAD = Cfg<HALO>::NLOAD;
+  using pipe::H;
+  using pipe::K;
+  using pipe::NZR;
+  using pipe::PS;
+  extern __shared__ __align__(16) float sm[];  // [NZR][PH][PW]
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int tilesx = g.nx / TX, tilesy = g.ny / TY;
+  int bid = blockIdx.x;
+  const int bx = bid % tilesx;
+  bid /= tilesx;
+  const int by = bid % tilesy;
+  bid /= tilesy;
+  const int z0 = bid * ZC;
+  const int x0 = bx * TX, y0 = by * TY;
+  const size_t F = g.F;
+  const size_t plane = (size_t)g.nx * g.ny;
+  const float* __restrict__ in = a.in[0];
+
+  auto psrc = [&](int pl) -> size_t { return (size_t)(g.zh ? pl + g.zh : (pl & (g.nz - 1))) * plane; };
+  // cp.async of input planes [pa, pb) into their ring slots (plane p -> slot p & (NZR-1))
+  auto load_planes = [&](int pa, int pb) {
+    const int n = (pb - pa) * pipe::NF4;
+    for (int i = threadIdx.x; i < n; i += 256) {
+      const int pl = pa + i / pipe::NF4, rem = i % pipe::NF4;
+      const int r = rem / (XW / 4), k = rem % (XW / 4);
+      const size_t src = psrc(pl) + (size_t)((y0 - H + r) & (g.ny - 1)) * g.nx + ((x0 - XH + 4 * k) & (g.nx - 1));
+      cp_async16(sm + (pl & (NZR - 1)) * PS + r * PW + 4 * k, in + src);
+    }
+  };
+  // steady-state stages load K planes = K * NF4 float4: thread t owns elements t + 256 j,
+  // whose plane offset, row / column source offset and smem offset are fixed
+  constexpr int NJ = (K * pipe::NF4 + 255) / 256;
+  int jps[NJ];  // (plane offset << 16) | smem offset, or -1
+  unsigned jrc[NJ];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int i = threadIdx.x + 256 * j, rem = i % pipe::NF4;
+    const int r = rem / (XW / 4), k = rem % (XW / 4);
+    jps[j] = i < K * pipe::NF4 ? ((i / pipe::NF4) << 16) | (r * PW + 4 * k) : -1;
+    jrc[j] = (unsigned)(((y0 - H + r) & (g.ny - 1)) * g.nx + ((x0 - XH + 4 * k) & (g.nx - 1)));
+  }
+  auto load_stage = [&](int pa) {  // planes [pa, pa + K)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      if (jps[j] < 0) continue;
+      const int pl = pa + (jps[j] >> 16);
+      cp_async16(sm + (pl & (NZR - 1)) * PS + (jps[j] & 0xffff), in + psrc(pl) + jrc[j]);
+    }
+  };
+
+  const int nst = ZC / K;
+  load_planes(z0 - H, z0 + K + H);  // stage 0
+  cp_commit();
+  if (nst > 1) load_stage(z0 + K + H);  // stage 1
+  cp_commit();
+
+  const size_t gi0 = (size_t)z0 * plane + (size_t)(y0 + ty) * g.nx + x0 + tx;
+  // per-point streams (delta_x, delta_y, delta_z, E), prefetched one plane ahead
+  float n0, n1, n2, nE = 1.0f;
+  auto fetch = [&](int zi) {
+    const size_t gi = gi0 + (size_t)zi * plane;
+    n0 = __ldg(a.delta + gi);
+    n1 = __ldg(a.delta + F + gi);
+    n2 = __ldg(a.delta + 2 * F + gi);
+    if (HAS_E) nE = __ldg(a.E + gi);
+  };
+  fetch(0);
+  double acc = 0.0;
+
+#pragma unroll 1
+  for (int st = 0; st < nst; ++st) {
+    cp_wait<1>();  // this stage's planes have landed (the next stage's may be in flight)
+    __syncthreads();
+#pragma unroll 1
+    for (int j = 0; j < K; ++j) {
+      const int zi = st * K + j, z = z0 + zi;
+      const size_t gi = gi0 + (size_t)zi * plane;
+      const float dx = n0, dy = n1, dz = n2, cE = nE;
+      if (zi + 1 < ZC) fetch(zi + 1);
+      const float fx = floorf(dx), fy = floorf(dy), fz = floorf(dz);
+      const int ix = (int)fx, iy = (int)fy, iz = (int)fz;
+      float r;
+      if (ix < -XH + 1 || ix > XH - 2 || iy < -H + 1 || iy > H - 2 || iz < -H + 1 || iz > H - 2) {
+        r = gather_global(g, in, x0 + tx, y0 + ty, z, dx, dy, dz);
+      } else {
+        float wx[4], wy[4], wz[4];
+        lag4(dx - fx, wx);
+        lag4(dy - fy, wy);
+        lag4(dz - fz, wz);
+        const int p0 = z + iz - 1;
+        gather_smem<1, 0>(sm, [&](int c) { return ((p0 + c) & (NZR - 1)) * PS; },
+                          (ty + iy - 1 + H) * PW + tx + ix - 1 + XH, wx, wy, wz, &r);
+      }
+      if (MODE == M_EFACTOR) {
+        const float bv = sm[(z & (NZR - 1)) * PS + (ty + H) * PW + tx + XH];  // divv(l)
+        a.out[0][gi] = 1.0f + a.sh * (r + bv) + a.h2 * r * bv;
+      } else {
+        float val = r;
+        if (HAS_E) val *= cE;
+        a.out[0][gi] = val;
+        if (MODE == M_LAST) {
+          const float res = __ldg(a.m1 + gi) - val;
+          if (a.lamS) a.lamS[gi] = res;
+          acc += (double)res * (double)res;
+        }
+      }
+    }
+    __syncthreads();  // every thread is done with the oldest K slots
+    if (st + 2 < nst) load_stage(z0 + (st + 2) * K + H);
+    cp_commit();
+  }
+  cp_wait<0>();
+
+  if (MODE == M_LAST) {
+    __shared__ double red[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < 8; ++w) s += red[w];
+      a.partials[blockIdx.x] = s;
+    }
+  }
+}
+
+// =====================================================================================
+// Trace: both RK2 midpoint feet of the 3 velocity components (R6), fused sum of v.
+// =====================================================================================
+template <int HALO>
+__global__ void __launch_bounds__(256, 2) k_sl_trace(Geom g, int ZC, TileArgs a) {
+  using namespace tiled;
+  constexpr int NF = 3;
+  constexpr int PS = Cfg<HALO>::PS, NZR = 2 * HALO + 2, NLOAD = Cfg<HALO>::PH * (XW / 4);
   extern __shared__ __align__(16) float sm[];  // [NF][NZR][PS]
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int tilesx = g.nx / TX, tilesy = g.ny / TY;
@@ -102,7 +303,6 @@ __global__ void __launch_bounds__(256) k_sl_tiled(Geom g, int ZC, TileArgs a) {
   const bool loader = threadIdx.x < NLOAD;
   const int ld_r = threadIdx.x / (XW / 4), ld_k = threadIdx.x % (XW / 4);
   const size_t ld_off = (size_t)((y0 - HALO + ld_r) & (g.ny - 1)) * g.nx + ((x0 - XH + 4 * ld_k) & (g.nx - 1));
-  // input plane p (slab-local, may be negative / past nz): periodic wrap, or the halo'd slab buffer
   auto pin = [&](int p) -> size_t { return (size_t)(g.zh ? p + g.zh : (p & (g.nz - 1))) * plane; };
   const int ld_s = ld_r * PW + 4 * ld_k;
 
@@ -117,15 +317,9 @@ __global__ void __launch_bounds__(256) k_sl_tiled(Geom g, int ZC, TileArgs a) {
   }
   __syncthreads();
 
-  double acc = 0.0, vs0 = 0.0, vs1 = 0.0, vs2 = 0.0;
+  double vs0 = 0.0, vs1 = 0.0, vs2 = 0.0;
   int slot0 = 0;  // ring slot of plane z - HALO
-  // per-point streams of the current plane, prefetched one plane ahead (hides HBM latency)
   const size_t gi0 = (size_t)z0 * plane + (size_t)(y0 + ty) * g.nx + x0 + tx;
-  float nd0 = 0.f, nd1 = 0.f, nd2 = 0.f, nE = 1.f;
-  if (MODE != M_TRACE) {
-    nd0 = __ldg(a.delta + gi0); nd1 = __ldg(a.delta + F + gi0); nd2 = __ldg(a.delta + 2 * F + gi0);
-    if (HAS_E) nE = __ldg(a.E + gi0);
-  }
 #pragma unroll 1
   for (int zi = 0; zi < ZC; ++zi) {
     const int z = z0 + zi;
@@ -136,91 +330,38 @@ __global__ void __launch_bounds__(256) k_sl_tiled(Geom g, int ZC, TileArgs a) {
 #pragma unroll
       for (int f = 0; f < NF; ++f) pre[f] = __ldg(reinterpret_cast<const float4*>(a.in[f] + po));
     }
-    const int x = x0 + tx, y = y0 + ty;
     const size_t gi = gi0 + (size_t)zi * plane;
-    const float cd0 = nd0, cd1 = nd1, cd2 = nd2, cE = nE;
-    if (MODE != M_TRACE && zi + 1 < ZC) {
-      const size_t gn = gi + plane;
-      nd0 = __ldg(a.delta + gn); nd1 = __ldg(a.delta + F + gn); nd2 = __ldg(a.delta + 2 * F + gn);
-      if (HAS_E) nE = __ldg(a.E + gn);
-    }
-
-    // gather NF fields at l + (dx, dy, dz) from the smem ring (or global fallback)
-    auto gather = [&](float dx, float dy, float dz, float* res) {
+    const int cidx = ((slot0 + HALO) % NZR) * PS + (ty + HALO) * PW + tx + XH;
+    const float u0 = sm[0 * NZR * PS + cidx];
+    const float u1 = sm[1 * NZR * PS + cidx];
+    const float u2 = sm[2 * NZR * PS + cidx];
+    vs0 += u0; vs1 += u1; vs2 += u2;
+    const float c0 = u0 * g.cx, c1 = u1 * g.cy, c2 = u2 * g.cz;
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      float* o = a.out[side];
+      if (!o) continue;
+      const float sg = side == 0 ? -1.0f : 1.0f;
+      const float dx = 0.5f * sg * c0, dy = 0.5f * sg * c1, dz = 0.5f * sg * c2;
       const float fx = floorf(dx), fy = floorf(dy), fz = floorf(dz);
       const int ix = (int)fx, iy = (int)fy, iz = (int)fz;
+      float r[NF];
       if (ix < -XH + 1 || ix > XH - 2 || iy < -HALO + 1 || iy > HALO - 2 || iz < -HALO + 1 || iz > HALO - 2) {
 #pragma unroll
-        for (int f = 0; f < NF; ++f) res[f] = gather_global(g, a.in[f], x, y, z, dx, dy, dz);
-        return;
-      }
-      float wx[4], wy[4], wz[4];
-      lag4(dx - fx, wx);
-      lag4(dy - fy, wy);
-      lag4(dz - fz, wz);
-      const int rowoff = (ty + iy - 1 + HALO) * PW + tx + ix - 1 + XH;
-      int s = slot0 + HALO + iz - 1;
-      if (s >= NZR) s -= NZR;
-#pragma unroll
-      for (int f = 0; f < NF; ++f) res[f] = 0.0f;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int pbase = s * PS + rowoff;
-#pragma unroll
-        for (int f = 0; f < NF; ++f) {
-          const float* pl = sm + f * NZR * PS + pbase;
-          float rc = 0.0f;
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const float* r = pl + b * PW;
-            float t = wx[0] * r[0];
-            t = fmaf(wx[1], r[1], t);
-            t = fmaf(wx[2], r[2], t);
-            t = fmaf(wx[3], r[3], t);
-            rc = fmaf(wy[b], t, rc);
-          }
-          res[f] = fmaf(wz[c], rc, res[f]);
-        }
-        if (++s == NZR) s = 0;
-      }
-    };
-
-    if (MODE == M_TRACE) {
-      const int cidx = ((slot0 + HALO) % NZR) * PS + (ty + HALO) * PW + tx + XH;
-      const float u0 = sm[0 * NZR * PS + cidx];
-      const float u1 = sm[1 * NZR * PS + cidx];
-      const float u2 = sm[2 * NZR * PS + cidx];
-      vs0 += u0; vs1 += u1; vs2 += u2;
-      const float c0 = u0 * g.cx, c1 = u1 * g.cy, c2 = u2 * g.cz;
-#pragma unroll
-      for (int side = 0; side < 2; ++side) {
-        float* o = a.out[side];
-        if (!o) continue;
-        const float sg = side == 0 ? -1.0f : 1.0f;
-        float r[NF];
-        gather(0.5f * sg * c0, 0.5f * sg * c1, 0.5f * sg * c2, r);
-        o[gi] = sg * g.cx * r[0];
-        o[F + gi] = sg * g.cy * r[1];
-        o[2 * F + gi] = sg * g.cz * r[2];
-      }
-    } else {
-      float r[NF];
-      gather(cd0, cd1, cd2, r);
-      if (MODE == M_EFACTOR) {
-        const float bv = sm[((slot0 + HALO) % NZR) * PS + (ty + HALO) * PW + tx + XH];  // divv(l)
-        a.out[0][gi] = 1.0f + a.sh * (r[0] + bv) + a.h2 * r[0] * bv;
+        for (int f = 0; f < NF; ++f) r[f] = gather_global(g, a.in[f], x0 + tx, y0 + ty, z, dx, dy, dz);
       } else {
-        float val = r[0];
-        if (HAS_E) val *= cE;
-        a.out[0][gi] = val;
-        if (MODE == M_LAST) {
-          const float res = a.m1[gi] - val;
-          if (a.lamS) a.lamS[gi] = res;
-          acc += (double)res * (double)res;
-        }
+        float wx[4], wy[4], wz[4];
+        lag4(dx - fx, wx);
+        lag4(dy - fy, wy);
+        lag4(dz - fz, wz);
+        const int s0 = slot0 + HALO + iz - 1;
+        gather_smem<NF, NZR * PS>(sm, [&](int c) { int s = s0 + c; if (s >= NZR) s -= NZR; return s * PS; },
+                                  (ty + iy - 1 + HALO) * PW + tx + ix - 1 + XH, wx, wy, wz, r);
       }
+      o[gi] = sg * g.cx * r[0];
+      o[F + gi] = sg * g.cy * r[1];
+      o[2 * F + gi] = sg * g.cz * r[2];
     }
-
     if (pf) {
       int ps = slot0 + 2 * HALO + 1;
       if (ps >= NZR) ps -= NZR;
@@ -231,7 +372,7 @@ __global__ void __launch_bounds__(256) k_sl_tiled(Geom g, int ZC, TileArgs a) {
     __syncthreads();
   }
 
-  if (MODE == M_TRACE && a.partials) {
+  if (a.partials) {
     __shared__ double redv[3][8];
     double v3[3] = {vs0, vs1, vs2};
 #pragma unroll
@@ -248,52 +389,75 @@ __global__ void __launch_bounds__(256) k_sl_tiled(Geom g, int ZC, TileArgs a) {
       a.partials[(size_t)threadIdx.x * kMaxPartials + blockIdx.x] = t;
     }
   }
-  if (MODE == M_LAST) {
-    __shared__ double red[8];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double s = 0.0;
-      for (int w = 0; w < 8; ++w) s += red[w];
-      a.partials[blockIdx.x] = s;
-    }
-  }
 }
 
+// ---- host side ------------------------------------------------------------------------
 bool tiled_ok(const Geom& g) {
   return g.d == 3 && g.nx >= tiled::TX && g.nx % tiled::TX == 0 && g.ny % tiled::TY == 0 &&
-         (g.zh ? g.nz >= 1 : g.nz >= 8);
+         g.nz % pipe::K == 0 && (g.zh ? g.nz >= pipe::K : g.nz >= 8);
 }
 
-static int tiled_zc(const Geom& g) {
-  int zc = g.nz < 64 ? g.nz : 64;
-  while (g.nz % zc) zc >>= 1;
-  return zc;
+static int num_sms_sl() {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    nsm = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return nsm;
 }
 
-int tiled_blocks(const Geom& g) { return (g.nx / tiled::TX) * (g.ny / tiled::TY) * (g.nz / tiled_zc(g)); }
+// z chunk per block (a multiple of `mult` dividing nz): balance the wave quantisation of
+// (tiles x chunks) blocks over the resident slots against the 2H-plane halo re-load.
+static int tiled_zc(const Geom& g, int H, int mult, int resident) {
+  int best = 0;
+  double bestc = 1e30;
+  for (int zc = 64; zc >= mult; zc >>= 1) {
+    if (zc > g.nz || g.nz % zc || zc % mult) continue;
+    const double blocks = (double)(g.nx / tiled::TX) * (g.ny / tiled::TY) * (g.nz / zc);
+    const double waves = blocks / resident, eff = waves / std::ceil(waves);
+    const double cost = (zc + 2.0 * H) / zc / eff;
+    if (cost < bestc) { bestc = cost; best = zc; }
+  }
+  return best ? best : mult;
+}
 
-template <int MODE, int NF, bool HAS_E, int HALO = 4>
-static void launch_tiled(const Geom& g, const TileArgs& a, cudaStream_t st) {
-  using C = tiled::Cfg<HALO>;
-  const size_t sm = (size_t)NF * C::NZR * C::PS * sizeof(float);
-  cudaFuncSetAttribute(k_sl_tiled<MODE, NF, HAS_E, HALO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_sl_tiled<MODE, NF, HAS_E, HALO><<<tiled_blocks(g), 256, sm, st>>>(g, tiled_zc(g), a);
+template <typename Kern>
+static int resident_blocks(Kern k, int threads, size_t smem) {
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem);
+  return (per_sm < 1 ? 1 : per_sm) * num_sms_sl();
+}
+
+template <int MODE, bool HAS_E>
+static int launch_pipe(const Geom& g, const TileArgs& a, cudaStream_t st) {
+  static int resident = 0;
+  if (!resident) resident = resident_blocks(k_sl_pipe<MODE, HAS_E>, 256, pipe::SMEM);
+  const int zc = tiled_zc(g, pipe::H, pipe::K, resident);
+  const int blocks = (g.nx / tiled::TX) * (g.ny / tiled::TY) * (g.nz / zc);
+  k_sl_pipe<MODE, HAS_E><<<blocks, 256, pipe::SMEM, st>>>(g, zc, a);
   count_launch();
+  return blocks;
 }
 
 void tiled_trace(const Geom& g, const float* v, float* df, float* da, double* vsum, int* nparts, cudaStream_t st) {
+  constexpr int HALO = 2;  // midpoint displacement dt/2 v: |floor| <= 1 (else L1 fallback)
   TileArgs a{};
   a.partials = vsum;
-  if (nparts) *nparts = tiled_blocks(g);
   // component stride of v: F, or F plus 2 zh halo planes for a halo'd slab copy
   const size_t cs = g.F + 2 * (size_t)g.zh * g.nx * g.ny;
   for (int c = 0; c < 3; ++c) a.in[c] = v + c * cs;
   a.out[0] = df;
   a.out[1] = da;
-  launch_tiled<M_TRACE, 3, false, 2>(g, a, st);  // midpoint displacement dt/2 v: |floor| <= 1
+  const size_t sm = (size_t)3 * (2 * HALO + 2) * tiled::Cfg<HALO>::PS * sizeof(float);
+  static int resident = 0;
+  if (!resident) resident = resident_blocks(k_sl_trace<HALO>, 256, sm);
+  const int zc = tiled_zc(g, HALO, 1, resident);
+  const int blocks = (g.nx / tiled::TX) * (g.ny / tiled::TY) * (g.nz / zc);
+  k_sl_trace<HALO><<<blocks, 256, sm, st>>>(g, zc, a);
+  count_launch();
+  if (nparts) *nparts = blocks;
 }
 
 void tiled_step(const Geom& g, const float* in, const float* delta, const float* E, float* out, cudaStream_t st) {
@@ -302,8 +466,8 @@ void tiled_step(const Geom& g, const float* in, const float* delta, const float*
   a.delta = delta;
   a.E = E;
   a.out[0] = out;
-  if (E) launch_tiled<M_STEP, 1, true>(g, a, st);
-  else launch_tiled<M_STEP, 1, false>(g, a, st);
+  if (E) launch_pipe<M_STEP, true>(g, a, st);
+  else launch_pipe<M_STEP, false>(g, a, st);
 }
 
 void tiled_last(const Geom& g, const float* in, const float* delta, const float* E, const float* m1, float* mS,
@@ -316,9 +480,7 @@ void tiled_last(const Geom& g, const float* in, const float* delta, const float*
   a.out[0] = mS;
   a.lamS = lamS;
   a.partials = partials;
-  *nparts = tiled_blocks(g);
-  if (E) launch_tiled<M_LAST, 1, true>(g, a, st);
-  else launch_tiled<M_LAST, 1, false>(g, a, st);
+  *nparts = E ? launch_pipe<M_LAST, true>(g, a, st) : launch_pipe<M_LAST, false>(g, a, st);
 }
 
 void tiled_efactor(const Geom& g, const float* divv, const float* delta, float sh, float h2, float* E,
@@ -329,7 +491,7 @@ void tiled_efactor(const Geom& g, const float* divv, const float* delta, float s
   a.out[0] = E;
   a.sh = sh;
   a.h2 = h2;
-  launch_tiled<M_EFACTOR, 1, false>(g, a, st);
+  launch_pipe<M_EFACTOR, false>(g, a, st);
 }
 
 }  // namespace topt
