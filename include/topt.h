@@ -182,6 +182,18 @@ topt_status topt_eval_gradient_host(topt_ctx* ctx, const float* m0_h, const floa
                                     const float* v_h, float* g_h, double* h_scalars,
                                     void* stream);
 
+/* Streaming form of topt_eval_gradient_host: ENQUEUES the copies of m0, m1, v, the
+ * evaluation and the copies of g and the scalars back, and returns.  The library runs
+ * them on its own copy-in, compute and copy-out streams with two device staging
+ * buffers, so the transfers of consecutive calls overlap the evaluation of the call in
+ * between; `stream` is made to wait for this call's results (the copy-in does not wait for
+ * earlier work on `stream`: the inputs are host data).  The host buffers must stay valid
+ * (inputs unmodified, outputs unread) until `stream` has been synchronised.
+ * Single slab (world == 1) only: TOPT_ERR_UNSUPPORTED otherwise. */
+topt_status topt_eval_gradient_host_async(topt_ctx* ctx, const float* m0_h, const float* m1_h,
+                                          const float* v_h, float* g_h, double* h_scalars,
+                                          void* stream);
+
 /* Forward-only objective (what an Armijo trial costs): d_scalars[OBJ, DIST,
  * REG] written (REG by Parseval). Asynchronous. */
 topt_status topt_objective(topt_ctx* ctx, const float* m0, const float* m1, const float* v,

@@ -148,6 +148,12 @@ class Topt:
         check(LIB.topt_eval_gradient_host(self.ctx, _ptr(m0_h), _ptr(m1_h), _ptr(v_h), _ptr(g_h),
                                           _ptr(scal_h), _stream()), "topt_eval_gradient_host")
 
+    def eval_gradient_host_async(self, m0_h, m1_h, v_h, g_h, scal_h):
+        """Host (pinned) buffers; enqueues and returns (results valid after the current
+        stream is synchronised).  Consecutive calls overlap transfers with evaluation."""
+        check(LIB.topt_eval_gradient_host_async(self.ctx, _ptr(m0_h), _ptr(m1_h), _ptr(v_h), _ptr(g_h),
+                                                _ptr(scal_h), _stream()), "topt_eval_gradient_host_async")
+
     def objective(self, m0, m1, v):
         m0, m1, v = (_f32(x, self.device) for x in (m0, m1, v))
         sc = torch.zeros(_lib.NSCALARS, dtype=torch.float64, device=self.device)

@@ -68,6 +68,7 @@ SIGNATURES = {
     "topt_set_step_replay": (_I, [_P, ctypes.POINTER(ctypes.c_double), _I]),
     "topt_eval_gradient": (_I, [_P, _P, _P, _P, _P, _P, _P, _P]),
     "topt_eval_gradient_host": (_I, [_P, _P, _P, _P, _P, _P, _P]),
+    "topt_eval_gradient_host_async": (_I, [_P, _P, _P, _P, _P, _P, _P]),
     "topt_objective": (_I, [_P, _P, _P, _P, _P, _P]),
     "topt_feet": (_I, [_P, _P, _P, _P, _P]),
     "topt_forward": (_I, [_P, _P, _P, _P, _P]),

@@ -222,6 +222,15 @@ topt_status topt_destroy(topt_ctx* ctx) {
   if (!ctx) return fail(TOPT_ERR_INVALID_ARG, "ctx is NULL");
   for (auto& r : ctx->recs) { ctx->pool.push_back(r.a); ctx->pool.push_back(r.b); }
   for (auto e : ctx->pool) cudaEventDestroy(e);
+  if (ctx->h_in) {
+    for (cudaStream_t x : {ctx->h_in, ctx->h_comp, ctx->h_out}) {
+      cudaStreamSynchronize(x);
+      cudaStreamDestroy(x);
+    }
+    cudaEventDestroy(ctx->ev_hfork);
+    for (int i = 0; i < 2; ++i)
+      for (cudaEvent_t e : {ctx->ev_hin[i], ctx->ev_hfree[i], ctx->ev_hdone[i], ctx->ev_hout[i]}) cudaEventDestroy(e);
+  }
   if (ctx->side) {
     cudaStreamSynchronize(ctx->side);
     cudaStreamDestroy(ctx->side);
@@ -942,6 +951,60 @@ topt_status topt_eval_gradient_host(topt_ctx* c, const float* m0_h, const float*
   if (g_h) TOPT_CUDA(cudaMemcpyAsync(g_h, sl.gcur, c->vecN * 4, cudaMemcpyDeviceToHost, st));
   TOPT_CUDA(cudaMemcpyAsync(h_scalars, sl.pub(4), TOPT_NSCALARS * 8, cudaMemcpyDeviceToHost, st));
   TOPT_CUDA(cudaStreamSynchronize(st));
+  return TOPT_OK;
+}
+
+// Two staging slots: slot 0 = (m0b, m1b, vb) -> (gcur, scur, scalar set 4), slot 1 =
+// (q[0, F), q[F, 2F), vt) -> (gq, sq, set 3) (solver vectors, idle outside topt_solve).
+// Per call, slot b:  h_in: wait free[b]; H2D; record in[b]  |  h_comp: wait in[b], out[b];
+// evaluate; record free[b], done[b]  |  h_out: wait done[b]; D2H; record out[b]  |
+// caller stream: wait out[b].
+topt_status topt_eval_gradient_host_async(topt_ctx* c, const float* m0_h, const float* m1_h, const float* v_h,
+                                          float* g_h, double* h_scalars, void* stream) {
+  topt_status s0 = need_ws(c);
+  if (s0 != TOPT_OK) return s0;
+  if (!m0_h || !m1_h || !v_h || !h_scalars) return fail(TOPT_ERR_INVALID_ARG, "NULL argument");
+  if (P_of(c) != 1) return fail(TOPT_ERR_UNSUPPORTED, "streaming host evaluation needs world == 1");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!c->h_in) {
+    TOPT_CUDA(cudaStreamCreateWithFlags(&c->h_in, cudaStreamNonBlocking));
+    TOPT_CUDA(cudaStreamCreateWithFlags(&c->h_comp, cudaStreamNonBlocking));
+    TOPT_CUDA(cudaStreamCreateWithFlags(&c->h_out, cudaStreamNonBlocking));
+    TOPT_CUDA(cudaEventCreateWithFlags(&c->ev_hfork, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) {
+      TOPT_CUDA(cudaEventCreateWithFlags(&c->ev_hin[i], cudaEventDisableTiming));
+      TOPT_CUDA(cudaEventCreateWithFlags(&c->ev_hfree[i], cudaEventDisableTiming));
+      TOPT_CUDA(cudaEventCreateWithFlags(&c->ev_hdone[i], cudaEventDisableTiming));
+      TOPT_CUDA(cudaEventCreateWithFlags(&c->ev_hout[i], cudaEventDisableTiming));
+    }
+  }
+  const int b = c->hslot;
+  c->hslot ^= 1;
+  Slab& sl = c->slabs[0];
+  float* m0d = b ? sl.q : sl.m0b;
+  float* m1d = b ? sl.q + sl.F : sl.m1b;
+  float* vd = b ? sl.vt : sl.vb;
+  const int set = b ? 3 : 4;
+  // the inputs are host buffers: the copy-in does not wait for earlier work on `stream`
+  // (which, after a previous call, ends with that call's copy-out), only for the slot
+  TOPT_CUDA(cudaStreamWaitEvent(c->h_in, c->ev_hfree[b], 0));
+  TOPT_CUDA(cudaMemcpyAsync(m0d, m0_h, c->F * 4, cudaMemcpyHostToDevice, c->h_in));
+  TOPT_CUDA(cudaMemcpyAsync(m1d, m1_h, c->F * 4, cudaMemcpyHostToDevice, c->h_in));
+  TOPT_CUDA(cudaMemcpyAsync(vd, v_h, c->vecN * 4, cudaMemcpyHostToDevice, c->h_in));
+  TOPT_CUDA(cudaEventRecord(c->ev_hin[b], c->h_in));
+  TOPT_CUDA(cudaStreamWaitEvent(c->h_comp, c->ev_hin[b], 0));
+  TOPT_CUDA(cudaStreamWaitEvent(c->h_comp, c->ev_hout[b], 0));
+  std::vector<Io> io = make_io(c, m0d, m1d, vd, set, c->h_comp);
+  if (b) { io[0].g = sl.gq; io[0].s = sl.sq; }
+  topt_status r = eval_gradient(c, io, c->h_comp);
+  if (r != TOPT_OK) return r;
+  TOPT_CUDA(cudaEventRecord(c->ev_hfree[b], c->h_comp));
+  TOPT_CUDA(cudaEventRecord(c->ev_hdone[b], c->h_comp));
+  TOPT_CUDA(cudaStreamWaitEvent(c->h_out, c->ev_hdone[b], 0));
+  if (g_h) TOPT_CUDA(cudaMemcpyAsync(g_h, io[0].g, c->vecN * 4, cudaMemcpyDeviceToHost, c->h_out));
+  TOPT_CUDA(cudaMemcpyAsync(h_scalars, sl.pub(set), TOPT_NSCALARS * 8, cudaMemcpyDeviceToHost, c->h_out));
+  TOPT_CUDA(cudaEventRecord(c->ev_hout[b], c->h_out));
+  TOPT_CUDA(cudaStreamWaitEvent(st, c->ev_hout[b], 0));
   return TOPT_OK;
 }
 

@@ -80,6 +80,10 @@ struct topt_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_div = nullptr, ev_u = nullptr;
   bool div_pending = false, u_pending = false;
+  // streaming host-buffer evaluations (topt_eval_gradient_host_async): two staging slots
+  cudaStream_t h_in = nullptr, h_comp = nullptr, h_out = nullptr;
+  cudaEvent_t ev_hfork = nullptr, ev_hin[2]{}, ev_hfree[2]{}, ev_hdone[2]{}, ev_hout[2]{};
+  int hslot = 0;
   // per-kernel-class timing (topt_profile / topt_kernel_stats)
   bool prof = false;
   struct Rec { int cls; cudaEvent_t a, b; double bytes; int launches; };
