@@ -698,7 +698,8 @@ void backward_half(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
 // inside both) everything stays on `st`.
 topt_status eval_gradient(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
   c->div_pending = c->u_pending = false;
-  if (P_of(c) == 1 && c->side && io[0].u == nullptr) {
+  // (profiling mode serialises everything on `st`, so the per-class times are standalone)
+  if (P_of(c) == 1 && c->side && io[0].u == nullptr && !c->prof) {
     cudaEventRecord(c->ev_fork, st);
     cudaStreamWaitEvent(c->side, c->ev_fork, 0);
     if (c->p.model != TOPT_INCOMPRESSIBLE) {

@@ -51,6 +51,9 @@ __device__ __forceinline__ float kprime(int q, int N) {  // Nyquist zeroed (R3)
 
 // values per thread: fp32 lines 16 (radix 16), fp64 lines and multi-field fp32 lines 8
 template <int N, int EMAX> struct Ev { static constexpr int v = N < EMAX ? N : EMAX; };
+// strided derivative lines: radix 16 (one smem exchange at N = 256) when summing time
+// slices, radix 8 (two exchanges, ~110 registers: 2 resident blocks instead of 1) for a
+// single field, where latency hiding needs the occupancy
 
 static int num_sms() {
   static int nsm = 0;
@@ -152,12 +155,13 @@ __global__ void __launch_bounds__(kThreads) k_rdx(Geom g, const float* __restric
 // line.  Thread (c, t), c fastest: every load / store of a row is one contiguous
 // 8*TXC-byte segment.
 // =====================================================================================
-template <int N>
-__global__ void __launch_bounds__(kThreads) k_rds(Geom g, int axis, int TXC, const float* __restrict__ psi,
-                                                  size_t psi_stride, const float* __restrict__ lam,
-                                                  size_t lam_stride, DerivWeights w, int J, float beta,
-                                                  float* __restrict__ out, int nitems) {
-  constexpr int E = Ev<N, 16>::v, T = N / E;
+template <int N, int EMAX>
+__global__ void __launch_bounds__(kThreads, (EMAX == 8 ? 2 : 1)) k_rds(Geom g, int axis, int TXC,
+                                                                       const float* __restrict__ psi,
+                                                                       size_t psi_stride, const float* __restrict__ lam,
+                                                                       size_t lam_stride, DerivWeights w, int J,
+                                                                       float beta, float* __restrict__ out, int nitems) {
+  constexpr int E = Ev<N, EMAX>::v, T = N / E;
   using R = RfCfg<N, E>;
   extern __shared__ __align__(16) float2 smem[];
   const int c = threadIdx.x % TXC, t = threadIdx.x / TXC;
@@ -216,11 +220,26 @@ __global__ void __launch_bounds__(kThreads) k_rds(Geom g, int axis, int TXC, con
   }
 }
 
+template <int N, int EMAX>
+static void rds_launch(const Geom& g, int axis, const DerivArgs& a, const DerivWeights& w, cudaStream_t st) {
+  constexpr int E = Ev<N, EMAX>::v, T = N / E;
+  using R = RfCfg<N, E>;
+  int TXC = kThreads / T;
+  if (2 * TXC > g.nx) TXC = g.nx / 2;
+  const int threads = TXC * T;
+  const size_t sm = (size_t)TXC * R::STRIDE * sizeof(float2);
+  const int outer = axis == 1 ? g.nz : g.ny;
+  const long long items = (long long)(g.nx / (2 * TXC)) * outer;
+  const int blocks = persistent_blocks(k_rds<N, EMAX>, threads, sm, items);
+  k_rds<N, EMAX><<<blocks, threads, sm, st>>>(g, axis, TXC, a.psi, a.psi_stride, a.lam, a.lam_stride, w, a.J, a.beta,
+                                              a.out, (int)items);
+}
+
 template <int N>
 static void deriv_dispatch(const Geom& g, int axis, const DerivArgs& a, const DerivWeights& w, cudaStream_t st) {
-  constexpr int E = Ev<N, 16>::v, T = N / E;
-  using R = RfCfg<N, E>;
   if (axis == 0) {
+    constexpr int E = Ev<N, 16>::v, T = N / E;
+    using R = RfCfg<N, E>;
     constexpr int LPB = kThreads / T;
     const size_t sm = (size_t)LPB * R::STRIDE * sizeof(float2);
     const size_t nreal = (size_t)g.ny * g.nz;
@@ -228,16 +247,10 @@ static void deriv_dispatch(const Geom& g, int axis, const DerivArgs& a, const De
     const int blocks = persistent_blocks(k_rdx<N>, kThreads, sm, groups);
     k_rdx<N><<<blocks, kThreads, sm, st>>>(g, a.psi, a.psi_stride, a.lam, a.lam_stride, w, a.J, a.beta, a.out,
                                             (int)groups);
+  } else if (a.J == 1) {
+    rds_launch<N, 8>(g, axis, a, w, st);   // single field (div v): occupancy first
   } else {
-    int TXC = kThreads / T;
-    if (2 * TXC > g.nx) TXC = g.nx / 2;
-    const int threads = TXC * T;
-    const size_t sm = (size_t)TXC * R::STRIDE * sizeof(float2);
-    const int outer = axis == 1 ? g.nz : g.ny;
-    const long long items = (long long)(g.nx / (2 * TXC)) * outer;
-    const int blocks = persistent_blocks(k_rds<N>, threads, sm, items);
-    k_rds<N><<<blocks, threads, sm, st>>>(g, axis, TXC, a.psi, a.psi_stride, a.lam, a.lam_stride, w, a.J, a.beta,
-                                          a.out, (int)items);
+    rds_launch<N, 16>(g, axis, a, w, st);  // time-slice sums: one smem exchange per FFT
   }
   count_launch();
 }
@@ -366,7 +379,7 @@ struct SpecOp {
 __device__ __forceinline__ double regL(double kk, int p) { return p == 1 ? kk : (p == 2 ? kk * kk : kk * kk * kk); }
 
 template <int N, int EMAX, int MODE, typename C>
-__global__ void __launch_bounds__(kThreads) k_rstrided(Geom g, int axis, int TXC, int NIN, int NOUT, ZList<C> Z,
+__global__ void __launch_bounds__(kThreads, (MODE >= 4 ? 1 : 2)) k_rstrided(Geom g, int axis, int TXC, int NIN, int NOUT, ZList<C> Z,
                                                        SpecOp op, int nitems) {
   constexpr int E = Ev<N, EMAX>::v, T = N / E;
   constexpr int NF = MODE >= 4 ? 3 : 1;  // fields held in registers

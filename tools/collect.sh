@@ -1,9 +1,9 @@
 #!/bin/bash
-# Round artefacts: full bench line, ncu launch list, ncu --set full of the SL step kernel.
-set -x
-python bench.py --steps 30 --warmup 5 > gpurun_out/bench_full.log 2>&1
+# Round artefacts: full bench line, ncu launch list of the same bench command, and
+# ncu --set full captures of the top kernels (each only after its command exited 0 without ncu).
+python bench.py --steps 30 --warmup 5 > gpurun_out/bench_full.log 2>&1 || { tail -20 gpurun_out/bench_full.log; exit 1; }
 tail -1 gpurun_out/bench_full.log > gpurun_out/bench_full.json
 B="python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e"
-$B > gpurun_out/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_ --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launch.log 2>&1
-ncu --set full --clock-control none --import-source on -k "regex:k_sl_tiled<0" -s 12 -c 3 -o gpurun_out/prof_slstep $B > gpurun_out/ncu_full.log 2>&1
-tail -2 gpurun_out/ncu_full.log
+$B > gpurun_out/plain.log 2>&1 || exit 1
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launch.log 2>&1
+bash tools/prof_multi.sh "k_sl_pipe<.int.0, .bool.1:4" "k_sl_trace:1" "k_rds:4" "k_rstrided<256, 8, 2, double2:0" "k_rdx:3" "k_rassemble:0"
