@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kThreads) k_rdx(Geom g, const float* __restric
   const int line = threadIdx.x / T, t = threadIdx.x % T;
   float2* lbuf = smem + line * R::STRIDE;
   float2 tw[R::NTW];
-  rf_tw<N, E, 1, 0>(tw, t);
+  rf_twiddles<N, E>(tw, t);
   const size_t nreal = (size_t)g.ny * g.nz;
   const float invN = 1.0f / (float)N;
   for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
@@ -155,8 +155,11 @@ __global__ void __launch_bounds__(kThreads) k_rdx(Geom g, const float* __restric
 // line.  Thread (c, t), c fastest: every load / store of a row is one contiguous
 // 8*TXC-byte segment.
 // =====================================================================================
+#ifndef TOPT_RDS16_MINB
+#define TOPT_RDS16_MINB 2
+#endif
 template <int N, int EMAX>
-__global__ void __launch_bounds__(kThreads, (EMAX == 8 ? 2 : 1)) k_rds(Geom g, int axis, int TXC,
+__global__ void __launch_bounds__(kThreads, (EMAX == 8 ? 2 : TOPT_RDS16_MINB)) k_rds(Geom g, int axis, int TXC,
                                                                        const float* __restrict__ psi,
                                                                        size_t psi_stride, const float* __restrict__ lam,
                                                                        size_t lam_stride, DerivWeights w, int J,
@@ -167,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, (EMAX == 8 ? 2 : 1)) k_rds(Geom g, i
   const int c = threadIdx.x % TXC, t = threadIdx.x / TXC;
   float2* lbuf = smem + c * R::STRIDE;
   float2 tw[R::NTW];
-  rf_tw<N, E, 1, 0>(tw, t);
+  rf_twiddles<N, E>(tw, t);
   const int tilesx = g.nx / (2 * TXC);
   const unsigned S = axis == 1 ? (unsigned)g.nx : (unsigned)g.nx * g.ny;
   const float invN = 1.0f / (float)N;
@@ -301,7 +304,7 @@ __global__ void __launch_bounds__(kThreads) k_rx_fwd(Geom g, RealIn in, ZList<C>
   const int line = threadIdx.x / T, t = threadIdx.x % T;
   C* lbuf = reinterpret_cast<C*>(smraw) + line * R::STRIDE;
   C tw[R::NTW];
-  rf_tw<N, E, 1, 0>(tw, t);
+  rf_twiddles<N, E>(tw, t);
   const size_t nrows = (size_t)g.ny * g.nz;
   const int f = blockIdx.y;
   const float* re = in.re[f];
@@ -336,7 +339,7 @@ __global__ void __launch_bounds__(kThreads) k_rx_inv(Geom g, ZList<C> Z, RealOut
   const int line = threadIdx.x / T, t = threadIdx.x % T;
   C* lbuf = reinterpret_cast<C*>(smraw) + line * R::STRIDE;
   C tw[R::NTW];
-  rf_tw<N, E, 1, 0>(tw, t);
+  rf_twiddles<N, E>(tw, t);
   const size_t nrows = (size_t)g.ny * g.nz;
   const int f = blockIdx.y;
   const C* Zf = Z.z[f];
@@ -389,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, (MODE >= 4 ? 1 : 2)) k_rstrided(Geom
   const int c = threadIdx.x % TXC, t = threadIdx.x / TXC;
   C* lbuf = reinterpret_cast<C*>(smraw) + c * R::STRIDE;
   C tw[R::NTW];
-  rf_tw<N, E, 1, 0>(tw, t);
+  rf_twiddles<N, E>(tw, t);
   const int tilesx = g.nx / TXC;
   const int outerN = axis == 1 ? g.nz : g.ny;
   const int tiles = tilesx * outerN;
@@ -530,12 +533,12 @@ template <int N, int LPR, bool LERAY>
 __global__ void __launch_bounds__(kThreads) k_rassemble(Geom g, AsmArgs a, int ngroups) {
   constexpr int E = Ev<N, (LPR >= 4 ? 8 : 16)>::v, T = N / E, LPB = kThreads / T;
   constexpr bool WARP = T <= 32;
-  using R = RfCfg<N, E>;
+  using R = RfCfg<N, E, true>;
   extern __shared__ __align__(16) float2 smem[];
   const int line = threadIdx.x / T, t = threadIdx.x % T;
   float2* lbuf = smem + line * R::STRIDE;
   float2 tw[R::NTW];
-  rf_tw<N, E, 1, 0>(tw, t);
+  rf_twiddles<N, E, true>(tw, t);
   const size_t nrows = (size_t)g.ny * g.nz;
   constexpr int pf = LERAY ? LPR / 2 : 0;  // first p field
   float vbar[3] = {0.f, 0.f, 0.f};
@@ -550,7 +553,7 @@ __global__ void __launch_bounds__(kThreads) k_rassemble(Geom g, AsmArgs a, int n
     for (int f = 0; f < LPR; ++f) {
 #pragma unroll
       for (int e = 0; e < E; ++e) z[f][e] = ok ? a.Z[f][o + T * e] : make_float2(0.f, 0.f);
-      rf_fft<N, E, true, WARP>(z[f], lbuf, t, tw);
+      rf_fft<N, E, true, WARP, true>(z[f], lbuf, t, tw);
     }
     if (!ok) continue;
 #pragma unroll

@@ -14,20 +14,30 @@
 // writes x'[(j/NS) NS R + k + q NS] (q < R).  Thread t owns butterflies j = t + b T
 // (b < E/R); its inputs are then positions t + T (b + r E/R) — the canonical layout — and
 // the outputs of the LAST stage (NS R = N) are positions t + T (b + q E/R), canonical again.
-// Twiddles of every stage after the first are loaded once per kernel into registers.
+// Twiddles: per stage after the first and per butterfly, only the base powers W^m, W^2m,
+// W^4m, W^8m (m = k N/(NS R), the ones below R) are loaded once per kernel into registers
+// (from the fp64-computed table); the other powers are composed on the fly, each a product
+// of at most three bases, so an fp32 twiddle carries at most a few ulps.
 #pragma once
 #include "fft.cuh"
 
 namespace topt {
 
 __host__ __device__ constexpr int rf_rad(int N, int E, int ns) { return (N / ns) < E ? N / ns : E; }
-// number of register twiddles from stage `ns` on
-__host__ __device__ constexpr int rf_ntw(int N, int E, int ns) {
-  return ns >= N ? 0 : (ns > 1 ? (E / rf_rad(N, E, ns)) * (rf_rad(N, E, ns) - 1) : 0) + rf_ntw(N, E, ns * rf_rad(N, E, ns));
+// twiddles kept per butterfly for radix R: all R-1 powers (FULL), or the base powers W^m
+// (R >= 2), W^2m (R >= 4), W^4m (R >= 8), W^8m (R >= 16)
+__host__ __device__ constexpr int rf_nb(int R, bool full) {
+  return full ? R - 1 : (R >= 16 ? 4 : (R >= 8 ? 3 : (R >= 4 ? 2 : 1)));
 }
-template <int N, int E> struct RfCfg {
+// number of register twiddles from stage `ns` on
+__host__ __device__ constexpr int rf_ntw(int N, int E, int ns, bool full) {
+  return ns >= N ? 0
+                 : (ns > 1 ? (E / rf_rad(N, E, ns)) * rf_nb(rf_rad(N, E, ns), full) : 0) +
+                       rf_ntw(N, E, ns * rf_rad(N, E, ns), full);
+}
+template <int N, int E, bool FULL = false> struct RfCfg {
   static constexpr int T = N / E;                                   // threads per line
-  static constexpr int NTW = rf_ntw(N, E, 1) > 0 ? rf_ntw(N, E, 1) : 1;
+  static constexpr int NTW = rf_ntw(N, E, 1, FULL) > 0 ? rf_ntw(N, E, 1, FULL) : 1;
   static constexpr int STRIDE = fft_line_stride(N);                 // smem complex per line
 };
 
@@ -35,22 +45,49 @@ template <typename C> __device__ __forceinline__ C rf_twid(int N, int m);
 template <> __device__ __forceinline__ float2 rf_twid<float2>(int N, int m) { return g_twiddle[N + m]; }
 template <> __device__ __forceinline__ double2 rf_twid<double2>(int N, int m) { return g_twiddle_d[N + m]; }
 
-// tw[OFF + b (R-1) + r - 1] = W_N^{r k N/(NS R)}, k = (t + b T) mod NS, for every stage NS > 1
-template <int N, int E, int NS, int OFF, typename C>
+// For every stage NS > 1 and butterfly b (m = k N/(NS R), k = (t + b T) mod NS):
+// FULL: tw[OFF + b (R-1) + r - 1] = W_N^{r m}; else tw[OFF + b nb + i] = W_N^{2^i m}.
+template <int N, int E, int NS, int OFF, bool FULL, typename C>
 __device__ __forceinline__ void rf_tw(C* tw, int t) {
   if constexpr (NS < N) {
-    constexpr int R = rf_rad(N, E, NS), B = E / R, T = N / E;
+    constexpr int R = rf_rad(N, E, NS), B = E / R, T = N / E, NB = rf_nb(R, FULL);
     if constexpr (NS > 1) {
 #pragma unroll
       for (int b = 0; b < B; ++b) {
-        const int k = (t + b * T) & (NS - 1);
+        const int m = ((t + b * T) & (NS - 1)) * (N / (NS * R));
 #pragma unroll
-        for (int r = 1; r < R; ++r) tw[OFF + b * (R - 1) + r - 1] = rf_twid<C>(N, (r * k * (N / (NS * R))) & (N - 1));
+        for (int i = 0; i < NB; ++i)
+          tw[OFF + b * NB + i] = rf_twid<C>(N, (FULL ? (i + 1) * m : (m << i)) & (N - 1));
       }
-      rf_tw<N, E, NS * R, OFF + B * (R - 1), C>(tw, t);
+      rf_tw<N, E, NS * R, OFF + B * NB, FULL, C>(tw, t);
     } else {
-      rf_tw<N, E, NS * R, OFF, C>(tw, t);
+      rf_tw<N, E, NS * R, OFF, FULL, C>(tw, t);
     }
+  }
+}
+template <int N, int E, bool FULL = false, typename C>
+__device__ __forceinline__ void rf_twiddles(C* tw, int t) {
+  rf_tw<N, E, 1, 0, FULL, C>(tw, t);
+}
+
+// w[r] = W^{r m} for r = 1 .. R-1 from the bases w1 = W^m, w2, w4, w8 (at most 3 products deep)
+template <int R, typename C>
+__device__ __forceinline__ void rf_powers(const C* base, C* w) {
+  w[1] = base[0];
+  if constexpr (R > 2) {
+    w[2] = base[1];
+    w[3] = cmul(w[2], w[1]);
+  }
+  if constexpr (R > 4) {
+    w[4] = base[2];
+    w[5] = cmul(w[4], w[1]);
+    w[6] = cmul(w[4], w[2]);
+    w[7] = cmul(w[4], w[3]);
+  }
+  if constexpr (R > 8) {
+    w[8] = base[3];
+#pragma unroll
+    for (int r = 9; r < 16; ++r) w[r] = cmul(w[8], w[r - 8]);
   }
 }
 
@@ -60,9 +97,9 @@ __device__ __forceinline__ void rf_sync() {
   else __syncthreads();
 }
 
-template <int N, int E, int NS, int OFF, bool INV, bool WARP, typename C>
+template <int N, int E, int NS, int OFF, bool INV, bool WARP, bool FULL, typename C>
 __device__ __forceinline__ void rf_stage(C (&a)[E], C* line, int t, const C* tw) {
-  constexpr int R = rf_rad(N, E, NS), B = E / R, T = N / E;
+  constexpr int R = rf_rad(N, E, NS), B = E / R, T = N / E, NB = rf_nb(R, FULL);
   constexpr bool LAST = NS * R == N;
   C o[E];
 #pragma unroll
@@ -71,11 +108,15 @@ __device__ __forceinline__ void rf_stage(C (&a)[E], C* line, int t, const C* tw)
 #pragma unroll
     for (int r = 0; r < R; ++r) x[r] = a[b + r * B];
     if constexpr (NS > 1) {
+      C w[R];
+      if constexpr (FULL) {
 #pragma unroll
-      for (int r = 1; r < R; ++r) {
-        const C w = tw[OFF + b * (R - 1) + r - 1];
-        x[r] = INV ? cmulconj(x[r], w) : cmul(x[r], w);
+        for (int r = 1; r < R; ++r) w[r] = tw[OFF + b * NB + r - 1];
+      } else {
+        rf_powers<R>(tw + OFF + b * NB, w);
       }
+#pragma unroll
+      for (int r = 1; r < R; ++r) x[r] = INV ? cmulconj(x[r], w[r]) : cmul(x[r], w[r]);
     }
     Dft<R, INV, C>::run(x);
 #pragma unroll
@@ -96,16 +137,16 @@ __device__ __forceinline__ void rf_stage(C (&a)[E], C* line, int t, const C* tw)
 #pragma unroll
     for (int e = 0; e < E; ++e) a[e] = line[fft_pad(t + T * e)];
     rf_sync<WARP>();
-    rf_stage<N, E, NS * R, OFF + (NS > 1 ? B * (R - 1) : 0), INV, WARP, C>(a, line, t, tw);
+    rf_stage<N, E, NS * R, OFF + (NS > 1 ? B * NB : 0), INV, WARP, FULL, C>(a, line, t, tw);
   }
 }
 
 // Unnormalised DFT of the line held in a[] (forward exp(-i k x), inverse exp(+i k x)).
-// `line` is this line's smem scratch (RfCfg::STRIDE complex); every thread of the sync
-// group (warp if WARP, else block) must call it.
-template <int N, int E, bool INV, bool WARP, typename C>
+// `line` is this line's smem scratch (RfCfg::STRIDE complex); `tw` from rf_twiddles with the
+// same FULL; every thread of the sync group (warp if WARP, else block) must call it.
+template <int N, int E, bool INV, bool WARP, bool FULL = false, typename C>
 __device__ __forceinline__ void rf_fft(C (&a)[E], C* line, int t, const C* tw) {
-  rf_stage<N, E, 1, 0, INV, WARP, C>(a, line, t, tw);
+  rf_stage<N, E, 1, 0, INV, WARP, FULL, C>(a, line, t, tw);
 }
 
 }  // namespace topt
