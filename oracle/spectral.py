@@ -173,6 +173,30 @@ def reg_value(grid: Grid, v, alpha: float, p: int) -> float:
     return 0.5 * alpha * inner(grid, v, apply_L(grid, v, p))
 
 
+def dft_coeff(grid: Grid, f, kvec) -> complex:
+    """One DFT coefficient f^_k = sum_l f_l exp(-i k . x_l), x_l = 2 pi l / n (R2), by
+    its plain definition, one axis at a time.  The phase k x_l = 2 pi ((k l) mod n) / n is
+    reduced in integers, so it is exact before the cos / sin (a high |k| times an inexact
+    x_l would carry a phase error that alpha |k|^{2p} amplifies).  kvec: integer
+    wavenumbers in paper order.  Used to check full-size spectral outputs at sampled modes."""
+    out = np.asarray(f, dtype=np.complex128)
+    for a in range(grid.d):  # paper axis a = numpy axis d-1-a; contract the last one each time
+        na = grid.n[a]
+        m = (int(kvec[a]) * np.arange(na, dtype=np.int64)) % na
+        out = out @ np.exp(-2j * np.pi * m / na)
+    return complex(out)
+
+
+def deriv_line(f_line):
+    """Spectral derivative of one periodic line on [0, 2pi): symbol i k' with the Nyquist
+    index zeroed (R3).  Used to check full-size derivative outputs on sampled lines."""
+    f_line = np.asarray(f_line, dtype=np.float64)
+    n = f_line.shape[-1]
+    k = np.fft.fftfreq(n, d=1.0 / n)
+    k[n // 2] = 0.0
+    return np.real(np.fft.ifft(1j * k * np.fft.fft(f_line, axis=-1), axis=-1))
+
+
 def gaussian_blur(grid: Grid, f, sigma_vox: float):
     """Spectral Gaussian smoothing with std sigma_vox*h_i.  Used by pins only."""
     mult = 1.0

@@ -1,0 +1,143 @@
+"""Full-size parity: BASELINE.json config 4 (256^3, continuity, nt = 8, H2, alpha = 1e-3) at
+v = v*, the configuration and launch geometry bench.py times.  The whole fp64 oracle
+evaluation at 256^3 takes minutes on the host, so every operator is checked on its own with
+the GPU's fp32 inputs to that operator (rounded once, handed to the oracle in fp64):
+  * feet (R5, R6) and one forward step with the Heun factor (R7), whole fields;
+  * lam^S = pi1 - pi^S (R1/R8) and adjoint steps (R8), whole fields;
+  * body force b = -sum_j w_j pi^j grad lam^j (R8, R10) on sampled x / y / z lines;
+  * g = alpha L v + b and s = -(alpha L~)^{-1} g at sampled Fourier modes,
+    by the DFT definition;
+  * dist, reg, <g, s>_h and ||g||_inf.
+Tolerance: relative L2 <= 1e-5 per operator (north_star)."""
+import numpy as np
+import pytest
+import torch
+
+from gpu_common import rel_l2
+from oracle import gradient as ogr
+from oracle import spectral, transport
+from oracle.interp import interp
+from oracle.spectral import Grid
+from synth import make_problem
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def run():
+    import paper_2510_08782_b200 as topt
+    d = make_problem(4, device="cuda:0")
+    n = tuple(d["n"])
+    assert n == (256, 256, 256)
+    f32 = lambda x: np.asarray(x, dtype=np.float32)
+    m0, m1, v = f32(d["m0"]), f32(d["m1"]), f32(d["vstar"])
+    t = topt.Topt(topt.Config(n=n, nt=d["nt"], model=d["model"], reg_order=d["reg_order"], alpha=d["alpha"],
+                              window=d["window"]), device="cuda:0")
+    dev = lambda x: torch.tensor(x, device="cuda:0")
+    g, s, sc = t.eval_gradient(dev(m0), dev(m1), dev(v))
+    lam, b = t.adjoint()
+    df, da = t.feet(dev(v))
+    traj = t.forward(dev(m0), dev(v))
+    torch.cuda.synchronize()
+    h = lambda x: x.double().cpu().numpy()
+    out = dict(d=d, grid=Grid(n), m0=m0.astype(np.float64), m1=m1.astype(np.float64), v=v.astype(np.float64),
+               g=h(g), s=h(s), sc=t.scalars_dict(sc), lam=h(lam), b=h(b), df=h(df), da=h(da), m=h(traj))
+    del t
+    torch.cuda.empty_cache()
+    return out
+
+
+def _ref_feet(run):
+    if "ref_feet" not in run:
+        run["ref_feet"] = transport.feet(run["grid"], run["v"], run["d"]["nt"])
+    return run["ref_feet"]
+
+
+def test_feet(run):
+    rf, ra = _ref_feet(run)
+    assert rel_l2(run["df"], rf) < TOL
+    assert rel_l2(run["da"], ra) < TOL
+
+
+def test_forward_steps(run):
+    grid, nt = run["grid"], run["d"]["nt"]
+    rf, _ = _ref_feet(run)
+    E = transport.source_factor_forward_continuity(grid, run["v"], rf, nt)
+    m = run["m"]
+    assert np.array_equal(m[0], run["m0"])
+    for j in (0, nt - 1):
+        ref = interp(m[j].astype(np.float32).astype(np.float64), rf) * E
+        assert rel_l2(m[j + 1], ref) < TOL, j
+
+
+def test_adjoint_steps(run):
+    grid, nt = run["grid"], run["d"]["nt"]
+    _, ra = _ref_feet(run)
+    lam, m = run["lam"], run["m"]
+    # fp32 subtraction of fp32 operands is the correctly rounded exact difference
+    np.testing.assert_array_equal(lam[nt], (run["m1"] - m[nt]).astype(np.float32))
+    for j in (nt - 1, 0):
+        ref = interp(lam[j + 1], ra)  # continuity adjoint: pure advection (R8)
+        assert rel_l2(lam[j], ref) < TOL, j
+
+
+def test_body_force_sampled_lines(run):
+    nt, lam, m, b = run["d"]["nt"], run["lam"], run["m"], run["b"]
+    w = ogr.trapezoid_weights(nt)
+    rng = np.random.default_rng(2510087824)
+    num, den = 0.0, 0.0
+    for a in range(3):  # paper axis a = numpy axis 2 - a
+        for _ in range(24):
+            i0, i1 = rng.integers(0, 256, size=2)
+            sl = [i0, i1]
+            sl.insert(2 - a, slice(None))
+            sl = tuple(sl)
+            ref = np.zeros(256)
+            for j in range(nt + 1):
+                ref -= w[j] * m[j][sl] * spectral.deriv_line(lam[j][sl])  # R8
+            num += np.sum((b[a][sl] - ref) ** 2)
+            den += np.sum(ref ** 2)
+    assert np.sqrt(num / den) < TOL
+
+
+def test_gradient_and_preconditioner_sampled_modes(run):
+    grid, d = run["grid"], run["d"]
+    alpha, p = d["alpha"], d["reg_order"]
+    rng = np.random.default_rng(2510087825)
+    ks = [(0, 0, 0), (1, 0, 0), (0, -3, 2), (128, 0, 0), (5, 128, -7), (128, 128, 128), (-60, 31, 90)]
+    ks += [tuple(int(x) for x in rng.integers(-127, 129, size=3)) for _ in range(10)]
+    ks += [tuple(int(x) for x in rng.integers(-8, 9, size=3)) for _ in range(10)]
+    gh, gref, sh, sref = [], [], [], []
+    for k in ks:
+        kk = float(sum(x * x for x in k))
+        L = kk ** p
+        Lt = L if L != 0.0 else 1.0  # kernel fix
+        vh = np.array([spectral.dft_coeff(grid, run["v"][c], k) for c in range(3)])
+        bh = np.array([spectral.dft_coeff(grid, run["b"][c], k) for c in range(3)])
+        g_k = np.array([spectral.dft_coeff(grid, run["g"][c], k) for c in range(3)])
+        s_k = np.array([spectral.dft_coeff(grid, run["s"][c], k) for c in range(3)])
+        gh.append(g_k); gref.append(alpha * L * vh + bh)
+        sh.append(s_k); sref.append(-g_k / (alpha * Lt))
+    gh, gref, sh, sref = map(np.array, (gh, gref, sh, sref))
+    assert np.linalg.norm(gh - gref) / np.linalg.norm(gref) < TOL
+    assert np.linalg.norm(sh - sref) / np.linalg.norm(sref) < TOL
+    # High |k| alone: there alpha L v dominates g and is the fp32 rounding noise of v amplified
+    # by alpha |k|^4 (an fp32 alpha L chain fails here).  Each mode of the fp32
+    # output g carries its own rounding noise, ~2^-24 rms(g) sqrt(N) per coefficient (4 sigma).
+    hi = [i for i, k in enumerate(ks) if sum(x * x for x in k) > 64 ** 2]
+    noise = 4 * 2.0 ** -24 * np.sqrt(np.mean(run["g"] ** 2)) * np.sqrt(grid.npts)
+    assert np.all(np.abs(gh[hi] - gref[hi]) <= noise + TOL * np.abs(gref[hi]))
+
+
+def test_scalars(run):
+    grid, d, sc = run["grid"], run["d"], run["sc"]
+    r = run["m"][-1] - run["m1"]
+    dist = 0.5 * spectral.inner(grid, r, r)
+    reg = spectral.reg_value(grid, run["v"], d["alpha"], d["reg_order"])
+    assert abs(sc["dist"] - dist) <= TOL * dist
+    assert abs(sc["reg"] - reg) <= TOL * reg
+    assert abs(sc["obj"] - (dist + reg)) <= TOL * (dist + reg)
+    gs = spectral.inner(grid, run["g"], run["s"])
+    assert abs(sc["gs"] - gs) <= TOL * abs(gs)
+    assert abs(sc["grad_inf"] - np.max(np.abs(run["g"]))) <= TOL * sc["grad_inf"]

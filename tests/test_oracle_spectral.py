@@ -141,3 +141,30 @@ def test_gaussian_blur_mode():
     x1, _ = g.coords()
     out = spectral.gaussian_blur(g, np.sin(x1), 1.0)
     np.testing.assert_allclose(out, np.exp(-0.5 * (2 * np.pi / 64) ** 2) * np.sin(x1), atol=1e-14)
+
+
+def test_dft_coeff_closed_form():
+    """f = cos(k0 . x + phi): f^_{k0} = (N/2) e^{i phi}, f^_{-k0} = (N/2) e^{-i phi}, 0 elsewhere."""
+    g = Grid((8, 6, 4))
+    x = g.coords()
+    k0, phi = (3, -2, 1), 0.7
+    f = np.cos(sum(k * xa for k, xa in zip(k0, x)) + phi)
+    N = g.npts
+    assert abs(spectral.dft_coeff(g, f, k0) - 0.5 * N * np.exp(1j * phi)) < 1e-10 * N
+    assert abs(spectral.dft_coeff(g, f, tuple(-k for k in k0)) - 0.5 * N * np.exp(-1j * phi)) < 1e-10 * N
+    for k in [(0, 0, 0), (3, 2, 1), (1, -2, 1), (3, -2, -1)]:
+        assert abs(spectral.dft_coeff(g, f, k)) < 1e-10 * N
+    # a constant: f^_0 = N c
+    assert abs(spectral.dft_coeff(g, np.full(g.shape, 2.5), (0, 0, 0)) - 2.5 * N) < 1e-10 * N
+
+
+def test_deriv_line_modes_and_nyquist():
+    n = 32
+    x = np.arange(n) * 2 * np.pi / n
+    np.testing.assert_allclose(spectral.deriv_line(np.sin(3 * x + 0.4)), 3 * np.cos(3 * x + 0.4), atol=1e-12)
+    np.testing.assert_allclose(spectral.deriv_line(np.cos(15 * x)), -15 * np.sin(15 * x), atol=1e-11)
+    assert np.max(np.abs(spectral.deriv_line(np.cos(16 * x)))) < 1e-12  # Nyquist zeroed (R3)
+    # rows of a 2D array are independent lines; brute-force O(n^2) DFT on random data
+    rng = np.random.default_rng(3)
+    f = rng.normal(size=(3, 16))
+    np.testing.assert_allclose(spectral.deriv_line(f), _brute_dft_deriv(f, 16, 1, 16), atol=1e-11)
