@@ -81,6 +81,38 @@ def _interp2(f, dx, dy):
     return out
 
 
+@numba.njit(parallel=True, cache=True)
+def _interp3_at(f, px, py, pz):
+    nz, ny, nx = f.shape
+    out = np.empty(px.shape[0])
+    for q in numba.prange(px.shape[0]):
+        ix = math.floor(px[q])
+        iy = math.floor(py[q])
+        iz = math.floor(pz[q])
+        wx = lagrange_weights(px[q] - ix)
+        wy = lagrange_weights(py[q] - iy)
+        wz = lagrange_weights(pz[q] - iz)
+        acc = 0.0
+        for c in range(4):
+            zz = (iz - 1 + c) % nz
+            for b in range(4):
+                yy = (iy - 1 + b) % ny
+                for a in range(4):
+                    xx = (ix - 1 + a) % nx
+                    acc += wz[c] * wy[b] * wx[a] * f[zz, yy, xx]
+        out[q] = acc
+    return out
+
+
+def interp_at(f, nodes, delta):
+    """I[f](l + delta) at a list of nodes only (3D): nodes int (3, M) in paper order
+    (x_1 index first), delta (3, M) displacements in cells.  The same formula as `interp`
+    one point at a time; used to check full-size fields at sampled points."""
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    pos = np.asarray(nodes, dtype=np.float64) + np.asarray(delta, dtype=np.float64)
+    return _interp3_at(f, np.ascontiguousarray(pos[0]), np.ascontiguousarray(pos[1]), np.ascontiguousarray(pos[2]))
+
+
 def interp(f, delta):
     """I[f](l + delta(l)) for every node l.
 

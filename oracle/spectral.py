@@ -179,11 +179,15 @@ def dft_coeff(grid: Grid, f, kvec) -> complex:
     reduced in integers, so it is exact before the cos / sin (a high |k| times an inexact
     x_l would carry a phase error that alpha |k|^{2p} amplifies).  kvec: integer
     wavenumbers in paper order.  Used to check full-size spectral outputs at sampled modes."""
-    out = np.asarray(f, dtype=np.complex128)
+    out = np.asarray(f)
     for a in range(grid.d):  # paper axis a = numpy axis d-1-a; contract the last one each time
         na = grid.n[a]
         m = (int(kvec[a]) * np.arange(na, dtype=np.int64)) % na
-        out = out @ np.exp(-2j * np.pi * m / na)
+        ang = 2.0 * np.pi * m / na
+        if np.iscomplexobj(out):
+            out = out @ (np.cos(ang) - 1j * np.sin(ang))
+        else:  # real field: first contraction in real arithmetic (cos and sin parts)
+            out = (out.astype(np.float64) @ np.cos(ang)) - 1j * (out.astype(np.float64) @ np.sin(ang))
     return complex(out)
 
 

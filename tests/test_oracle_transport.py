@@ -200,3 +200,17 @@ def test_adjoint_duality_advection():
         return abs(a - b) / abs(a)
 
     assert err(E) < 2e-2 and err(2.0 - E) > 5 * err(E)
+
+
+def test_interp_at_equals_field_interp_at_the_same_nodes():
+    """Point-list interpolation = the whole-field routine (pinned above) at those nodes."""
+    from oracle.interp import interp, interp_at
+    rng = np.random.default_rng(7)
+    f = rng.normal(size=(8, 12, 16))
+    delta = rng.uniform(-3.5, 3.5, size=(3,) + f.shape)
+    full = interp(f, delta)
+    idx = rng.integers(0, 8 * 12 * 16, size=50)
+    k, j, i = np.unravel_index(idx, f.shape)
+    nodes = np.stack([i, j, k])
+    got = interp_at(f, nodes, delta[:, k, j, i])
+    np.testing.assert_array_equal(got, full[k, j, i])
