@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(kThreads) k_rdx(Geom g, const float* __restric
 #define TOPT_RDS16_MINB 2
 #endif
 template <int N, int EMAX>
-__global__ void __launch_bounds__(kThreads, (EMAX == 8 ? 2 : TOPT_RDS16_MINB)) k_rds(Geom g, int axis, int TXC,
+__global__ void __launch_bounds__(kThreads, (EMAX == 8 || N == 256 ? TOPT_RDS16_MINB : 1)) k_rds(Geom g, int axis, int TXC,
                                                                        const float* __restrict__ psi,
                                                                        size_t psi_stride, const float* __restrict__ lam,
                                                                        size_t lam_stride, DerivWeights w, int J,
