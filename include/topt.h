@@ -199,6 +199,15 @@ topt_status topt_eval_gradient_host_async(topt_ctx* ctx, const float* m0_h, cons
 topt_status topt_objective(topt_ctx* ctx, const float* m0, const float* m1, const float* v,
                            double* d_scalars, void* stream);
 
+/* Flow-map diagnostics (figure captions; reading R32): the
+ * map y (foot at t = 0 of the characteristic ending at x at t = 1) as the composition of
+ * the n_t backward semi-Lagrangian maps with the static RK2 foot, and det(grad y) by
+ * spectral differentiation of the periodic displacement.  v: d*F device input;
+ * y_disp: d*F device output, y(x) - x in radians; det: F device output.  Single slab
+ * (world == 1) only: TOPT_ERR_UNSUPPORTED otherwise.  Asynchronous; uses the workspace
+ * (do not overlap with an evaluation on another stream). */
+topt_status topt_flow_map(topt_ctx* ctx, const float* v, float* y_disp, float* det, void* stream);
+
 /* ---- operator entry points (per-operator parity) ----------------------------------- */
 
 /* Characteristic feet as displacements in cells (R5, R6): delta_f = X - x (forward),

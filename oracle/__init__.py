@@ -23,8 +23,10 @@ Modules
              direction (2.5)/(2.6)  (P:25-29, P:105-108, P:160-175)
   solver     Armijo with memory, FP map q (2.7), NGMRES(w) Alg.1, AA(w)
              Alg.2, GA-NGMRES(w;sigma,tau) Alg.3 (P:152-263)
+  flowmap    flow map y and det(grad y) (figure captions P:323, P:781, P:866;
+             reading R32)
 
 Parity pins: every function is pinned by tests in ``tests/test_oracle_*.py``
 against closed forms, invariants and brute force.
 """
-from . import spectral, interp, transport, gradient, solver  # noqa: F401
+from . import spectral, interp, transport, gradient, solver, flowmap  # noqa: F401

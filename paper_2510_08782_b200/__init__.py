@@ -160,6 +160,14 @@ class Topt:
         check(LIB.topt_objective(self.ctx, _ptr(m0), _ptr(m1), _ptr(v), _ptr(sc), _stream()), "topt_objective")
         return self.scalars_dict(sc)
 
+    # -- diagnostics
+    def flow_map(self, v):
+        """(y - x in radians (d, *shape), det(grad y) (*shape)) — reading R32."""
+        v = _f32(v, self.device)
+        y, det = self._vec(), self._fld()
+        check(LIB.topt_flow_map(self.ctx, _ptr(v), _ptr(y), _ptr(det), _stream()), "topt_flow_map")
+        return y, det
+
     # -- operators
     def feet(self, v):
         v = _f32(v, self.device)

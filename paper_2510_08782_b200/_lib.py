@@ -69,6 +69,7 @@ SIGNATURES = {
     "topt_eval_gradient": (_I, [_P, _P, _P, _P, _P, _P, _P, _P]),
     "topt_eval_gradient_host": (_I, [_P, _P, _P, _P, _P, _P, _P]),
     "topt_eval_gradient_host_async": (_I, [_P, _P, _P, _P, _P, _P, _P]),
+    "topt_flow_map": (_I, [_P, _P, _P, _P, _P]),
     "topt_objective": (_I, [_P, _P, _P, _P, _P, _P]),
     "topt_feet": (_I, [_P, _P, _P, _P, _P]),
     "topt_forward": (_I, [_P, _P, _P, _P, _P]),

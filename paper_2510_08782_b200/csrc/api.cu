@@ -1112,6 +1112,37 @@ topt_status topt_derivative(topt_ctx* c, const float* f, int32_t axis, float* ou
   return TOPT_OK;
 }
 
+// Flow map y and det(grad y) (figure captions; reading R32): the
+// displacement u = y - x is composed over the n_t backward SL maps with the static RK2
+// foot, u^{j+1} = delta_f + I[u^j](l + delta_f); J[b][a] = d_a (h_b u_b) by the spectral
+// derivative kernels; det(I + J) pointwise (fp64 arithmetic on fp32 J).
+topt_status topt_flow_map(topt_ctx* c, const float* v, float* y_disp, float* det, void* stream) {
+  topt_status s0 = single_slab(c);
+  if (s0 != TOPT_OK) return s0;
+  if (!v || !y_disp || !det) return fail(TOPT_ERR_INVALID_ARG, "NULL argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  Slab& sl = c->slabs[0];
+  const int d = c->d, S = c->p.nt;
+  launch_trace(sl.g, v, sl.df, nullptr, nullptr, nullptr, st);
+  float* ua = sl.utmp;
+  float* ub = sl.b;
+  TOPT_CUDA(cudaMemsetAsync(ua, 0, c->vecN * 4, st));
+  for (int j = 0; j < S; ++j) {
+    launch_flow_step(sl.g, ua, sl.df, ub, st);
+    std::swap(ua, ub);
+  }
+  float* J = reinterpret_cast<float*>(sl.Zv);  // d*d fields of F (Zv holds 12 F floats)
+  for (int b = 0; b < d; ++b)
+    for (int a = 0; a < d; ++a) {
+      const double hb = c->h[b];
+      DerivArgs da{ua + (size_t)b * sl.F, 0, nullptr, 0, &hb, 1, 0.f, J + (size_t)(b * d + a) * sl.F};
+      launch_deriv_accum(sl.g, a, da, st);
+    }
+  launch_flow_det(sl.g, ua, J, c->h, y_disp, det, st);
+  TOPT_CHECK_LAUNCH();
+  return TOPT_OK;
+}
+
 topt_status topt_apply_precond(topt_ctx* c, const float* g, float* s, void* stream) {
   topt_status s0 = single_slab(c);
   if (s0 != TOPT_OK) return s0;

@@ -61,6 +61,12 @@ void launch_sl_last(const Geom& g, const float* in, const float* delta, const fl
 void launch_efactor(const Geom& g, const float* divv, const float* delta, float sgn_half_dt,
                     float half_dt2, float* E, cudaStream_t st);
 
+// flow map (R32): u_out = delta + I[u_in](l + delta) (d components, cells); det(I + J) with
+// J[b][a] = d_a (h_b u_b) (d*d fields) and the physical displacement h_b u_b
+void launch_flow_step(const Geom& g, const float* uin, const float* delta, float* uout, cudaStream_t st);
+void launch_flow_det(const Geom& g, const float* u, const float* J, const double* h, float* ydisp, float* det,
+                     cudaStream_t st);
+
 // shared-memory z-marching variants (kernels_sl_tiled.cu), used when tiled_ok(g)
 bool tiled_ok(const Geom& g);
 void tiled_trace(const Geom& g, const float* v, float* df, float* da, double* vsum, int* nparts, cudaStream_t st);

@@ -194,6 +194,59 @@ __global__ void __launch_bounds__(kThreads) k_efactor(Geom g, const float* __res
   }
 }
 
+// Flow map (R32): one composition step of the backward map, all d displacement components
+// with one stencil: u_out_c(l) = delta_c(l) + I[u_in_c](l + delta(l))  (cells).
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_flow_step(Geom g, const float* __restrict__ uin,
+                                                        const float* __restrict__ delta,
+                                                        float* __restrict__ uout) {
+  const size_t F = g.F;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < F; i += (size_t)gridDim.x * blockDim.x) {
+    int x, y, z;
+    coords(g, i, x, y, z);
+    const float d0 = delta[i], d1 = delta[F + i], d2 = D == 3 ? delta[2 * F + i] : 0.0f;
+    Stencil<D> st;
+    st.build(g, x, y, z, d0, d1, d2);
+    uout[i] = d0 + st.apply(uin);
+    uout[F + i] = d1 + st.apply(uin + F);
+    if (D == 3) uout[2 * F + i] = d2 + st.apply(uin + 2 * F);
+  }
+}
+
+// det(I + J) with J[b][a] = d/dx_a (h_b u_b) given as d*d fields (row b, column a);
+// also writes the physical displacement y_b - x_b = h_b u_b.
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_flow_det(Geom g, const float* __restrict__ u,
+                                                       const float* __restrict__ J, float hx, float hy,
+                                                       float hz, float* __restrict__ ydisp,
+                                                       float* __restrict__ det) {
+  const size_t F = g.F;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < F; i += (size_t)gridDim.x * blockDim.x) {
+    if (D == 2) {
+      const double a = 1.0 + J[i], b = J[F + i], c = J[2 * F + i], e = 1.0 + J[3 * F + i];
+      det[i] = (float)(a * e - b * c);
+      ydisp[i] = hx * u[i];
+      ydisp[F + i] = hy * u[F + i];
+    } else {
+      double m[3][3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) m[r][q] = (r == q ? 1.0 : 0.0) + J[(size_t)(3 * r + q) * F + i];
+      det[i] = (float)(m[0][0] * (m[1][1] * m[2][2] - m[1][2] * m[2][1]) -
+                       m[0][1] * (m[1][0] * m[2][2] - m[1][2] * m[2][0]) +
+                       m[0][2] * (m[1][0] * m[2][1] - m[1][1] * m[2][0]));
+      ydisp[i] = hx * u[i];
+      ydisp[F + i] = hy * u[F + i];
+      ydisp[2 * F + i] = hz * u[2 * F + i];
+    }
+  }
+}
+
+void launch_flow_step(const Geom& g, const float* uin, const float* delta, float* uout, cudaStream_t st);
+void launch_flow_det(const Geom& g, const float* u, const float* J, const double* h, float* ydisp, float* det,
+                     cudaStream_t st);
+
 int grid_for(size_t n, int threads, int max_blocks) {
   size_t b = (n + threads - 1) / threads;
   if (b > (size_t)max_blocks) b = max_blocks;
@@ -249,6 +302,21 @@ void launch_sl_last(const Geom& g, const float* in, const float* delta, const fl
     if (E) k_sl_last<2, true><<<gr, kThreads, 0, st>>>(g, in, delta, E, m1, mS, lamS, partials);
     else k_sl_last<2, false><<<gr, kThreads, 0, st>>>(g, in, delta, E, m1, mS, lamS, partials);
   }
+  count_launch();
+}
+
+void launch_flow_step(const Geom& g, const float* uin, const float* delta, float* uout, cudaStream_t st) {
+  if (g.d == 3) k_flow_step<3><<<sl_grid(g), kThreads, 0, st>>>(g, uin, delta, uout);
+  else k_flow_step<2><<<sl_grid(g), kThreads, 0, st>>>(g, uin, delta, uout);
+  count_launch();
+}
+
+void launch_flow_det(const Geom& g, const float* u, const float* J, const double* h, float* ydisp, float* det,
+                     cudaStream_t st) {
+  if (g.d == 3)
+    k_flow_det<3><<<sl_grid(g), kThreads, 0, st>>>(g, u, J, (float)h[0], (float)h[1], (float)h[2], ydisp, det);
+  else
+    k_flow_det<2><<<sl_grid(g), kThreads, 0, st>>>(g, u, J, (float)h[0], (float)h[1], 0.f, ydisp, det);
   count_launch();
 }
 

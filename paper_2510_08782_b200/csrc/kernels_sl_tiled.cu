@@ -137,9 +137,13 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 // =====================================================================================
 // Single-field pipelined kernel (STEP / LAST / EFACTOR).
 // =====================================================================================
+#ifndef TOPT_SL_HALO
+#define TOPT_SL_HALO 4
+#endif
 namespace pipe {
-constexpr int H = 4, K = 4;         // y/z halo; planes per pipeline stage
-constexpr int NZR = 2 * H + 2 * K;  // 16 ring slots (power of two)
+constexpr int H = TOPT_SL_HALO, K = 4;  // y/z halo; planes per pipeline stage
+constexpr int NZR = 16;                 // ring slots (power of two, >= 2H + 2K)
+static_assert(NZR >= 2 * H + 2 * K, "ring too small");
 constexpr int PS = tiled::Cfg<H>::PS, PH = tiled::Cfg<H>::PH;
 constexpr int NF4 = PH * (tiled::XW / 4);  // float4 per plane
 constexpr size_t SMEM = (size_t)NZR * PS * sizeof(float);
