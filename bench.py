@@ -342,6 +342,41 @@ def run_topt(args):
                "h2d_bytes_per_step": int(4 * npts * (2 + len(d["n"]))),
                "d2h_bytes_per_step": int(4 * npts * len(d["n"]) + 16 * 8)}
 
+    # GA-NGMRES iterations (Armijo trials, Gram inner products, host LSQ,
+    # mixing, stop test) on the same problem from v^0 = 0, after freeing the evaluation context
+    solver = None
+    if args.solver_iters > 0:
+        del t
+        torch.cuda.empty_cache()
+        kw = dict(window=d["window"], sigma=d.get("sigma", 1), tau=d.get("tau", 0), max_iter=args.solver_iters,
+                  eps_rel=0.0, **cfgp)
+        if slab:  # a fresh NCCL unique id per communicator
+            uid2 = share_unique_id(rank, world, topt.get_unique_id)
+            ts = topt.Topt(topt.Config(**kw), device=dev, rank=rank, world=world, unique_id=uid2)
+        else:
+            ts = topt.Topt(topt.Config(**kw), device=dev)
+        ts.solve(m0, m1)  # warm-up
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, rep = ts.solve(m0, m1)
+        torch.cuda.synchronize()
+        sec = max_over_ranks(time.perf_counter() - t0, world, dev)
+        ts.profile(True)
+        ts.solve(m0, m1)
+        st = {x["name"]: x for x in ts.kernel_stats()}
+        ts.profile(False)
+        gbs = lambda k: round(st[k]["bytes"] / (st[k]["ms"] / 1e3) / 1e9, 1) if st.get(k, {}).get("ms") else None
+        F = npts * 4.0
+        solver = {"method": f"GA-NGMRES(w={kw['window']}; sigma={kw['sigma']}, tau={kw['tau']})",
+                  "iterations": rep["iters"], "wall_s": round(sec, 4),
+                  "ms_per_iteration": round(1e3 * sec / max(1, rep["iters"]), 3),
+                  "iterations_per_s": round(rep["iters"] / sec, 3),
+                  "grad_evals": rep["grad_evals"], "obj_evals": rep["obj_evals"],
+                  "ls_share": round(rep["t_ls"] / rep["t_total"], 4) if rep["t_total"] else None,
+                  "gram_GB/s": gbs("ngmres_gram"), "mix_GB/s": gbs("ngmres_mix"),
+                  "ngmres_step_bytes_model": (3 * (kw["window"] + 2) + 4) * len(d["n"]) * F}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         sec, _ = oracle_eval_rate(args.cpu_n, str(dev))
@@ -370,6 +405,7 @@ def run_topt(args):
             "hbm_frac_pass_model": round(model_bytes * (value if slab else value / world) / (peak * 1e9), 4),
             "pass_model_bytes_per_eval": model_bytes,
             "kernels": breakdown,
+            "solver": solver,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -387,6 +423,7 @@ def main():
     ap.add_argument("--cpu-n", type=int, default=128, help="oracle sample grid for cpu_baseline")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--solver-iters", type=int, default=4, help="GA-NGMRES iterations timed (0: skip)")
     ap.add_argument("--parallel", default="slab", choices=["slab", "replica"],
                     help="N > 1: z-slabs over NCCL (one problem) or independent replicas")
     args = ap.parse_args()

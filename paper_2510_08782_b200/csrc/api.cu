@@ -319,10 +319,10 @@ namespace {
 // each result written once per launch group).  K_SL_STEP: every interior SL
 // step of both sweeps (one kernel); the last forward step (fused mismatch) is its own class.
 enum KClass { K_TRACE, K_SL_STEP, K_SL_LAST, K_EFACTOR, K_DIV, K_BODY, K_VCHAIN, K_BCHAIN, K_ASSEMBLE, K_COMM,
-              K_MISC, K_NCLASS };
+              K_MISC, K_GRAM, K_MIX, K_NCLASS };
 const char* kClassNames[K_NCLASS] = {"sl_trace",   "sl_step",        "sl_step_last", "efactor",  "div_v",
                                      "body_force", "vchain_alphaLv", "bchain_fft",   "assemble", "comm",
-                                     "misc"};
+                                     "misc",       "ngmres_gram",    "ngmres_mix"};
 
 cudaEvent_t take_event(topt_ctx* c) {
   if (!c->pool.empty()) {
@@ -819,7 +819,10 @@ topt_status host_dots(topt_ctx* c, std::function<const float*(Slab&)> a,
     std::vector<const float*> b;
     for (auto& f : bs) b.push_back(f(sl));
     int np = 0;
-    launch_multidot(a(sl), b.data(), n, c->vecN, sl.partials, &np, st);
+    {
+      Prof pr(c, K_GRAM, (n + 1.0) * c->vecN * 4.0, 1, st);  // a and every b read once (a8)
+      launch_multidot(a(sl), b.data(), n, c->vecN, sl.partials, &np, st);
+    }
     launch_finalize_multi(sl.partials, 0, n, np, 1.0, sl.dots, st);
     dd.push_back(sl.dots);
   }
@@ -1389,6 +1392,7 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
     for (auto& sl : c->slabs) {
       std::vector<const float*> p;
       for (auto& f : vs) p.push_back(f(sl));
+      Prof pr(c, K_MIX, (p.size() + 2.0) * V * 4.0, 1, st);  // q and every v read, out written (a10)
       launch_mix(q(sl), p.data(), beta.data(), (int)p.size(), V, out(sl), st);
     }
   };
