@@ -223,6 +223,117 @@ __global__ void __launch_bounds__(kThreads, (EMAX == 8 || N == 256 ? TOPT_RDS16_
   }
 }
 
+// Body force along a strided axis (J time slices): as k_rds, but the psi tile of slice j+1
+// and the lam tile of slice j are copied global -> shared with cp.async while slice j is
+// transformed, so the HBM latency of both streams hides behind the line FFTs (no extra
+// registers).  Tiles are [N rows][TXC column pairs] (8*TXC bytes per row).
+__device__ __forceinline__ void cp_async16_f(void* smem, const float* g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g));
+}
+__device__ __forceinline__ void cp_commit_f() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_wait1_f() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_wait0_f() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+template <int N, int EMAX>
+__global__ void __launch_bounds__(kThreads, (N == 256 ? TOPT_RDS16_MINB : 1)) k_rds_pf(
+    Geom g, int axis, int TXC, const float* __restrict__ psi, size_t psi_stride, const float* __restrict__ lam,
+    size_t lam_stride, DerivWeights w, int J, float beta, float* __restrict__ out, int nitems) {
+  constexpr int E = Ev<N, EMAX>::v, T = N / E;
+  using R = RfCfg<N, E>;
+  extern __shared__ __align__(16) float2 smem[];
+  const int c = threadIdx.x % TXC, t = threadIdx.x / TXC;
+  float2* lbuf = smem + c * R::STRIDE;
+  float2* Pt = smem + TXC * R::STRIDE;  // psi tile
+  float2* Lt = Pt + N * TXC;            // lam tile
+  float2 tw[R::NTW];
+  rf_twiddles<N, E>(tw, t);
+  const int tilesx = g.nx / (2 * TXC);
+  const unsigned S = axis == 1 ? (unsigned)g.nx : (unsigned)g.nx * g.ny;
+  const float invN = 1.0f / (float)N;
+  const int half = TXC / 2, nchunk = N * half;  // 16-byte chunks per tile
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int x0 = (item % tilesx) * 2 * TXC, outer = item / tilesx;
+    const unsigned tile0 = (axis == 1 ? ((unsigned)outer << (g.lx + g.ly)) : ((unsigned)outer << g.lx)) + x0;
+    const unsigned base = tile0 + 2 * c;
+    auto issue = [&](float2* dst, const float* field) {
+      for (int i = threadIdx.x; i < nchunk; i += blockDim.x) {
+        const int row = i / half, k = i % half;
+        cp_async16_f(dst + row * TXC + 2 * k, field + tile0 + row * S + 4 * k);
+      }
+    };
+    float2 acc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = make_float2(0.f, 0.f);
+    issue(Pt, psi);
+    cp_commit_f();
+    for (int j = 0; j < J; ++j) {
+      if (lam) issue(Lt, lam + j * lam_stride);
+      cp_commit_f();
+      cp_wait1_f();  // psi_j has landed (lam_j may be in flight)
+      __syncthreads();
+      float2 z[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) z[e] = Pt[(t + T * e) * TXC + c];
+      __syncthreads();  // the psi tile is free
+      if (j + 1 < J) issue(Pt, psi + (j + 1) * psi_stride);
+      cp_commit_f();
+      rf_fft<N, E, false, false>(z, lbuf, t, tw);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const float k = kprime(t + T * e, N) * invN;
+        z[e] = make_float2(-k * z[e].y, k * z[e].x);
+      }
+      rf_fft<N, E, true, false>(z, lbuf, t, tw);
+      const float wj = w.w[j];
+      cp_wait1_f();  // lam_j has landed (psi_{j+1} may be in flight)
+      __syncthreads();
+      if (lam) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const float2 l = Lt[(t + T * e) * TXC + c];
+          acc[e].x = fmaf(wj * l.x, z[e].x, acc[e].x);
+          acc[e].y = fmaf(wj * l.y, z[e].y, acc[e].y);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          acc[e].x = fmaf(wj, z[e].x, acc[e].x);
+          acc[e].y = fmaf(wj, z[e].y, acc[e].y);
+        }
+      }
+      __syncthreads();  // the lam tile is free
+    }
+    cp_wait0_f();
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      float2* o = reinterpret_cast<float2*>(out + base + (t + T * e) * S);
+      float2 r = acc[e];
+      if (beta != 0.0f) {
+        const float2 p = *o;
+        r.x += beta * p.x;
+        r.y += beta * p.y;
+      }
+      *o = r;
+    }
+  }
+}
+
+template <int N, int EMAX>
+static void rds_pf_launch(const Geom& g, int axis, const DerivArgs& a, const DerivWeights& w, cudaStream_t st) {
+  constexpr int E = Ev<N, EMAX>::v, T = N / E;
+  using R = RfCfg<N, E>;
+  int TXC = kThreads / T;
+  if (2 * TXC > g.nx) TXC = g.nx / 2;
+  const int threads = TXC * T;
+  const size_t sm = ((size_t)TXC * R::STRIDE + 2 * (size_t)N * TXC) * sizeof(float2);
+  const int outer = axis == 1 ? g.nz : g.ny;
+  const long long items = (long long)(g.nx / (2 * TXC)) * outer;
+  const int blocks = persistent_blocks(k_rds_pf<N, EMAX>, threads, sm, items);
+  k_rds_pf<N, EMAX><<<blocks, threads, sm, st>>>(g, axis, TXC, a.psi, a.psi_stride, a.lam, a.lam_stride, w, a.J,
+                                                 a.beta, a.out, (int)items);
+}
+
 template <int N, int EMAX>
 static void rds_launch(const Geom& g, int axis, const DerivArgs& a, const DerivWeights& w, cudaStream_t st) {
   constexpr int E = Ev<N, EMAX>::v, T = N / E;
@@ -253,7 +364,11 @@ static void deriv_dispatch(const Geom& g, int axis, const DerivArgs& a, const De
   } else if (a.J == 1) {
     rds_launch<N, 8>(g, axis, a, w, st);   // single field (div v): occupancy first
   } else {
-    rds_launch<N, 16>(g, axis, a, w, st);  // time-slice sums: one smem exchange per FFT
+    // time-slice sums: one smem exchange per FFT; at N >= 512 (one resident block per SM)
+    // the tiles of the next slice are prefetched with cp.async (measured: +7% at 512^3,
+    // -10% at 256^3 where two blocks per SM already overlap the loads)
+    if constexpr (N >= 512) rds_pf_launch<N, 16>(g, axis, a, w, st);
+    else rds_launch<N, 16>(g, axis, a, w, st);
   }
   count_launch();
 }
