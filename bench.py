@@ -326,15 +326,18 @@ def run_topt(args):
         vh = torch.tensor(vn, dtype=torch.float32).pin_memory()
         gh = torch.empty_like(vh).pin_memory()
         sch = torch.zeros(16, dtype=torch.float64).pin_memory()
+        # one slab: the streaming call (transfers of step k+-1 overlap step k); z-slabs over NCCL:
+        # the synchronous call (the library's copy streams are single-slab)
+        host_eval = t.eval_gradient_host if slab else t.eval_gradient_host_async
         for _ in range(max(1, args.warmup)):
-            t.eval_gradient_host_async(m0h, m1h, vh, gh, sch)
+            host_eval(m0h, m1h, vh, gh, sch)
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for _ in range(args.steps):  # every step: H2D m0, m1, v; evaluate; D2H g + scalars
-            t.eval_gradient_host_async(m0h, m1h, vh, gh, sch)
+            host_eval(m0h, m1h, vh, gh, sch)
         f1.record(stream)
         torch.cuda.synchronize()
         ems = max_over_ranks(f0.elapsed_time(f1), world, dev)
