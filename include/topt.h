@@ -93,6 +93,9 @@ typedef struct {
   int32_t exit;               /* topt_exit */
   int32_t ngmres_steps;       /* accelerated steps taken */
   double t_total, t_pde, t_ls; /* seconds: time to solution, PDE evaluations, LSQ (host) */
+  double t_q, t_f;              /* seconds: computing q(v^k) (Armijo trials + g(q)); evaluating
+                                   the mixed iterate (the paper's q and f timer columns) */
+  double dist0;                 /* dist at v^0 (the paper's "dist" column is dist / dist0) */
 } topt_report;
 
 typedef struct topt_ctx topt_ctx;

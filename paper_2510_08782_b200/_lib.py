@@ -46,6 +46,7 @@ class Report(ctypes.Structure):
         ("iters", ctypes.c_int32), ("grad_evals", ctypes.c_int32), ("obj_evals", ctypes.c_int32),
         ("pde_solves", ctypes.c_int32), ("exit", ctypes.c_int32), ("ngmres_steps", ctypes.c_int32),
         ("t_total", ctypes.c_double), ("t_pde", ctypes.c_double), ("t_ls", ctypes.c_double),
+        ("t_q", ctypes.c_double), ("t_f", ctypes.c_double), ("dist0", ctypes.c_double),
     ]
 
     def as_dict(self):

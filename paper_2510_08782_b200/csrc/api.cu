@@ -1261,7 +1261,7 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
   const size_t nsl = c->slabs.size();
   std::memset(rep, 0, sizeof(*rep));
   const double t0 = now();
-  double t_pde = 0.0, t_ls = 0.0;
+  double t_pde = 0.0, t_ls = 0.0, t_q = 0.0, t_f = 0.0;
   int grad_evals = 0, obj_evals = 0, nsteps = 0;
   std::deque<double> replay(c->replay.begin(), c->replay.end());
   topt_status r;
@@ -1346,6 +1346,7 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
   t_pde += now() - te;
   const double g0 = cur.pub(TOPT_S_GRAD_INF);
   rep->grad_inf0 = g0;
+  rep->dist0 = cur.pub(TOPT_S_DIST);
   if (!aa && (r = push(Vc, Gc, Uc, true)) != TOPT_OK) return r;
 
   // q-state helpers: v_q = v + rho s, u_q = u - rho (g - gbar)
@@ -1440,6 +1441,7 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
       }
     }
     t_pde += now() - te;
+    t_q += now() - te;
     if (!accepted) {
       exit_code = TOPT_STAGNATED;
       break;
@@ -1452,6 +1454,7 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
       te = now();
       if ((r = eval_into(Q, Uq, Gq, Sq, 2, qs)) != TOPT_OK) return r;  // g(q): both branches (R17)
       t_pde += now() - te;
+      t_q += now() - te;
       if (fp_step) {
         accept_q();
       } else {
@@ -1484,6 +1487,7 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
         te = now();
         if ((r = eval_new()) != TOPT_OK) return r;
         t_pde += now() - te;
+        t_f += now() - te;
         ++nsteps;
       }
       (void)wk;
@@ -1522,12 +1526,14 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
         te = now();
         if ((r = eval_new()) != TOPT_OK) return r;
         t_pde += now() - te;
+        t_f += now() - te;
         ++nsteps;
       } else {
         if ((r = push(Vt, Q, Uq, false)) != TOPT_OK) return r;
         te = now();
         if ((r = eval_into(Q, Uq, Gq, Sq, 2, qs)) != TOPT_OK) return r;
         t_pde += now() - te;
+        t_q += now() - te;
         accept_q();
       }
     }
@@ -1561,6 +1567,8 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
   rep->t_total = now() - t0;
   rep->t_pde = t_pde;
   rep->t_ls = t_ls;
+  rep->t_q = t_q;
+  rep->t_f = t_f;
   return TOPT_OK;
 }
 
