@@ -222,6 +222,12 @@ topt_status topt_destroy(topt_ctx* ctx) {
   if (!ctx) return fail(TOPT_ERR_INVALID_ARG, "ctx is NULL");
   for (auto& r : ctx->recs) { ctx->pool.push_back(r.a); ctx->pool.push_back(r.b); }
   for (auto e : ctx->pool) cudaEventDestroy(e);
+  for (auto& ge : ctx->graphs) cudaGraphExecDestroy(ge.exec);
+  if (ctx->gcap) {
+    cudaStreamSynchronize(ctx->gcap);
+    cudaStreamDestroy(ctx->gcap);
+    cudaEventDestroy(ctx->ev_gcap);
+  }
   if (ctx->h_in) {
     for (cudaStream_t x : {ctx->h_in, ctx->h_comp, ctx->h_out}) {
       cudaStreamSynchronize(x);
@@ -257,6 +263,8 @@ topt_status topt_bind_workspace(topt_ctx* c, void* dptr, size_t bytes) {
   if (bytes < c->ws_need) return fail(TOPT_ERR_WORKSPACE, "workspace too small");
   c->ws = (char*)dptr;
   c->ws_bytes = bytes;
+  for (auto& ge : c->graphs) cudaGraphExecDestroy(ge.exec);  // they bake the old workspace in
+  c->graphs.clear();
   const int world = c->world;
   for (int si = 0; si < c->comm.nloc; ++si) {
     Slab& sl = c->slabs[si];
@@ -913,6 +921,53 @@ std::vector<Io> make_io(topt_ctx* c, const float* m0, const float* m1, const flo
 // ======================================================================================
 extern "C" {
 
+// Replay a captured evaluation for this pointer key, capturing it on first use: the work
+// `body(stream)` is recorded on the library's capture stream (the caller's stream may be the
+// legacy default stream, which cannot capture), instantiated once and launched on `st`.
+// One slab only (no host decisions, no collectives); profiling mode runs eagerly.
+static const int kMaxGraphs = 16;
+static bool graphs_ok(topt_ctx* c) { return c->use_graphs && !c->prof && c->comm.P == 1; }
+static topt_status graph_run(topt_ctx* c, const void* const key[8], cudaStream_t st,
+                             const std::function<topt_status(cudaStream_t)>& body) {
+  for (auto& ge : c->graphs)
+    if (std::equal(ge.key, ge.key + 8, key)) {
+      TOPT_CUDA(cudaGraphLaunch(ge.exec, st));
+      launch_count_add(ge.nlaunch);
+      return TOPT_OK;
+    }
+  if (!c->gcap) {
+    TOPT_CUDA(cudaStreamCreateWithFlags(&c->gcap, cudaStreamNonBlocking));
+    TOPT_CUDA(cudaEventCreateWithFlags(&c->ev_gcap, cudaEventDisableTiming));
+  }
+  const long long l0 = launch_count();
+  TOPT_CUDA(cudaStreamBeginCapture(c->gcap, cudaStreamCaptureModeRelaxed));
+  topt_status r = body(c->gcap);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(c->gcap, &graph);
+  if (r != TOPT_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return r;
+  }
+  if (ec != cudaSuccess) return fail(TOPT_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ei != cudaSuccess) return fail(TOPT_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei));
+  topt_ctx::GraphEntry ge;
+  std::copy(key, key + 8, ge.key);
+  ge.exec = exec;
+  ge.nlaunch = launch_count() - l0;
+  launch_count_add(-ge.nlaunch);  // captured, not launched
+  if ((int)c->graphs.size() >= kMaxGraphs) {
+    cudaGraphExecDestroy(c->graphs.front().exec);
+    c->graphs.erase(c->graphs.begin());
+  }
+  c->graphs.push_back(ge);
+  TOPT_CUDA(cudaGraphLaunch(exec, st));
+  launch_count_add(ge.nlaunch);
+  return TOPT_OK;
+}
+
 topt_status topt_eval_gradient(topt_ctx* c, const float* m0, const float* m1, const float* v, float* g, float* s,
                                double* d_scalars, void* stream) {
   topt_status s0 = need_ws(c);
@@ -921,6 +976,18 @@ topt_status topt_eval_gradient(topt_ctx* c, const float* m0, const float* m1, co
   if (!aligned16(m0) || !aligned16(m1) || !aligned16(v) || (g && !aligned16(g)) || (s && !aligned16(s)))
     return fail(TOPT_ERR_INVALID_ARG, "pointers must be 16-byte aligned");
   cudaStream_t st = (cudaStream_t)stream;
+  if (graphs_ok(c)) {
+    const void* key[8] = {(const void*)1, m0, m1, v, g, s, d_scalars, nullptr};
+    return graph_run(c, key, st, [&](cudaStream_t cs) -> topt_status {
+      std::vector<Io> io = make_io(c, m0, m1, v, 4, cs);
+      io[0].g = g;
+      io[0].s = s;
+      io[0].scal = d_scalars;
+      topt_status rr = eval_gradient(c, io, cs);
+      TOPT_CHECK_LAUNCH();
+      return rr;
+    });
+  }
   std::vector<Io> io = make_io(c, m0, m1, v, 4, st);
   if (!emu(c)) {
     io[0].g = g;
@@ -998,14 +1065,21 @@ topt_status topt_eval_gradient_host_async(topt_ctx* c, const float* m0_h, const 
   TOPT_CUDA(cudaEventRecord(c->ev_hin[b], c->h_in));
   TOPT_CUDA(cudaStreamWaitEvent(c->h_comp, c->ev_hin[b], 0));
   TOPT_CUDA(cudaStreamWaitEvent(c->h_comp, c->ev_hout[b], 0));
-  std::vector<Io> io = make_io(c, m0d, m1d, vd, set, c->h_comp);
-  if (b) { io[0].g = sl.gq; io[0].s = sl.sq; }
-  topt_status r = eval_gradient(c, io, c->h_comp);
+  float* gd = b ? sl.gq : sl.gcur;
+  float* sd = b ? sl.sq : sl.scur;
+  auto body = [&](cudaStream_t cs) -> topt_status {
+    std::vector<Io> io = make_io(c, m0d, m1d, vd, set, cs);
+    io[0].g = gd;
+    io[0].s = sd;
+    return eval_gradient(c, io, cs);
+  };
+  const void* key[8] = {(const void*)2, m0d, m1d, vd, gd, sd, sl.pub(set), nullptr};
+  topt_status r = graphs_ok(c) ? graph_run(c, key, c->h_comp, body) : body(c->h_comp);
   if (r != TOPT_OK) return r;
   TOPT_CUDA(cudaEventRecord(c->ev_hfree[b], c->h_comp));
   TOPT_CUDA(cudaEventRecord(c->ev_hdone[b], c->h_comp));
   TOPT_CUDA(cudaStreamWaitEvent(c->h_out, c->ev_hdone[b], 0));
-  if (g_h) TOPT_CUDA(cudaMemcpyAsync(g_h, io[0].g, c->vecN * 4, cudaMemcpyDeviceToHost, c->h_out));
+  if (g_h) TOPT_CUDA(cudaMemcpyAsync(g_h, gd, c->vecN * 4, cudaMemcpyDeviceToHost, c->h_out));
   TOPT_CUDA(cudaMemcpyAsync(h_scalars, sl.pub(set), TOPT_NSCALARS * 8, cudaMemcpyDeviceToHost, c->h_out));
   TOPT_CUDA(cudaEventRecord(c->ev_hout[b], c->h_out));
   TOPT_CUDA(cudaStreamWaitEvent(st, c->ev_hout[b], 0));
@@ -1359,8 +1433,12 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
     }
   };
   auto eval_into = [&](Acc v, Acc u, Acc g, Acc s, int set, HostScalars& out) -> topt_status {
-    std::vector<Io> io = io_at(v, u, g, s, set);
-    topt_status rr = eval_gradient(c, io, st);
+    auto body = [&](cudaStream_t cs) -> topt_status { std::vector<Io> io = io_at(v, u, g, s, set);
+                                                      return eval_gradient(c, io, cs); };
+    Slab& s0 = c->slabs[0];
+    const void* key[8] = {(const void*)3, m0s[0], m1s[0], v(s0), u ? u(s0) : nullptr, g(s0), s(s0),
+                          (const void*)(intptr_t)set};
+    topt_status rr = graphs_ok(c) ? graph_run(c, key, st, body) : body(st);
     if (rr != TOPT_OK) return rr;
     ++grad_evals;
     return fetch(c, set, out, st);
@@ -1416,9 +1494,12 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
     } else {
       for (int t = 0; t <= P.max_backtracks; ++t) {
         make_q(rho_t);
-        std::vector<Io> io = io_at(Q, nullptr, nullptr, nullptr, 1);
-        forward_half(c, io, false, st);
-        TOPT_CHECK_LAUNCH();
+        auto body = [&](cudaStream_t cs) -> topt_status { std::vector<Io> io = io_at(Q, nullptr, nullptr, nullptr, 1);
+                                                          forward_half(c, io, false, cs);
+                                                          TOPT_CHECK_LAUNCH();
+                                                          return TOPT_OK; };
+        const void* key[8] = {(const void*)4, m0s[0], m1s[0], Q(c->slabs[0]), nullptr, nullptr, nullptr, nullptr};
+        if ((r = graphs_ok(c) ? graph_run(c, key, st, body) : body(st)) != TOPT_OK) return r;
         ++obj_evals;
         HostScalars ts;
         r = fetch(c, 1, ts, st);

@@ -84,6 +84,13 @@ struct topt_ctx {
   cudaStream_t h_in = nullptr, h_comp = nullptr, h_out = nullptr;
   cudaEvent_t ev_hfork = nullptr, ev_hin[2]{}, ev_hfree[2]{}, ev_hdone[2]{}, ev_hout[2]{};
   int hslot = 0;
+  // CUDA graphs of topt_eval_gradient / topt_objective, keyed by their pointers (a captured
+  // evaluation is replayed with one cudaGraphLaunch; the workspace binding is baked in)
+  struct GraphEntry { const void* key[8]; cudaGraphExec_t exec; long long nlaunch; };
+  std::vector<GraphEntry> graphs;
+  cudaStream_t gcap = nullptr;  // capture stream (the caller's may be the legacy stream)
+  cudaEvent_t ev_gcap = nullptr;
+  bool use_graphs = true;
   // per-kernel-class timing (topt_profile / topt_kernel_stats)
   bool prof = false;
   struct Rec { int cls; cudaEvent_t a, b; double bytes; int launches; };

@@ -45,6 +45,7 @@ struct VecList { const float* p[kMaxVecs]; float c[kMaxVecs]; };
 void upload_twiddles();
 void count_launch();          // one per kernel launch (all wrappers)
 long long launch_count();
+void launch_count_add(long long n);  // graph replays add the kernels they contain
 
 // ---- semi-Lagrangian kernels (kernels_sl.cu) --------------------------------------
 // Feet; when vsum_partials != null also per-block sums of v_c into slots 0..d-1 (*nparts blocks)

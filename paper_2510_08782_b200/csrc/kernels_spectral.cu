@@ -25,6 +25,9 @@
 
 #include <cmath>
 #include <cstdio>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "internal.cuh"
 #include "rfft.cuh"
@@ -66,12 +69,32 @@ static int num_sms() {
 }
 
 // persistent grid: resident blocks of `kern`, capped by the number of work items
+// resident blocks per SM of (kernel, threads, smem), queried once (host API calls are
+// microseconds each: at small grids they would dominate the launch path)
 template <typename K>
-static int persistent_blocks(K kern, int threads, size_t smem, long long items) {
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+static int resident_per_sm(K kern, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, size_t>, int> cache;
+  static std::map<const void*, size_t> smem_set;  // the attribute only ever grows per kernel
+  const auto key = std::make_tuple((const void*)kern, threads, smem);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  size_t& cur = smem_set[(const void*)kern];
+  if (smem > cur) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cur = smem;
+  }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
   if (per_sm < 1) per_sm = 1;
+  cache[key] = per_sm;
+  return per_sm;
+}
+
+template <typename K>
+static int persistent_blocks(K kern, int threads, size_t smem, long long items) {
+  const int per_sm = resident_per_sm(kern, threads, smem);
   long long b = (long long)num_sms() * per_sm;
   if (b > items) b = items;
   if (b < 1) b = 1;

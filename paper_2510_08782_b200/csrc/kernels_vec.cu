@@ -14,6 +14,7 @@ namespace topt {
 static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 long long launch_count() { return g_launches.load(); }
+void launch_count_add(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 // dst = scale * (sum or max) of partials[slot * kMaxPartials + 0 .. nparts-1]
 __global__ void k_finalize(const double* __restrict__ partials, int nparts, double scale, int is_max,
