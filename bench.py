@@ -312,6 +312,7 @@ def run_topt(args):
                 "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                 "algorithmic_bytes_per_launch": per_launch_bytes, "peak_kind": peak_kind,
                 "share_of_step": round(dom["ms"] / total_ms, 4) if total_ms else None}
+    profile_ms_per_step = total_ms / args.steps  # kernels serialised (no side-stream overlap)
     breakdown = {x["name"]: {"share": round(x["ms"] / total_ms, 4),
                              "GB/s": round(x["bytes"] / (x["ms"] / 1e3) / 1e9, 1) if x["bytes"] else None,
                              "launches_per_step": x["launches"] / args.steps} for x in kern}
@@ -408,6 +409,7 @@ def run_topt(args):
             "hbm_frac_pass_model": round(model_bytes * (value if slab else value / world) / (peak * 1e9), 4),
             "pass_model_bytes_per_eval": model_bytes,
             "kernels": breakdown,
+            "profile_ms_per_step_serialised": round(profile_ms_per_step, 4),
             "solver": solver,
         }
         print(json.dumps(line), flush=True)

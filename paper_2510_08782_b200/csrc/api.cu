@@ -505,6 +505,22 @@ void run_vchain(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
   }
 }
 
+// Merged v/b chain (kernels_spectral.cu gchain_*): one slab, non-Leray, u not supplied and
+// not wanted by the caller.  Only the forward transform of v runs in fp64; g^ = alpha L v^ +
+// b^ and p^ are formed at the last-axis pass and share the fp32 inverse passes.
+bool merged_chain(const topt_ctx* c, const std::vector<Io>& io) {
+  return c->comm.P == 1 && c->p.model != TOPT_INCOMPRESSIBLE && io[0].u == nullptr && !c->want_u;
+}
+// fp64 forward x (and y) passes of v into Zv
+void vchain_fwd(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
+  const double F = (double)c->F, d = c->d, half = c->d == 3 ? 2.0 : 1.0;
+  Prof pr(c, K_VCHAIN, d * 4.0 * F + half * 16.0 * F + (c->d == 3 ? 2.0 * half * 16.0 * F : 0.0), c->d == 3 ? 2 : 1,
+          st);
+  Slab& sl = c->slabs[0];
+  double2* Z[3] = {sl.Zv, sl.Zv + sl.F, sl.Zv + 2 * sl.F};
+  vchain_xy(sl.g, io[0].v, Z, false, st);
+}
+
 // Forward half: feet (R6), static factor (continuity, R7), m^0..m^S, lam^S = m1 - m^S
 // (R1/R8), dist -> scal[DIST], sum_x v_c -> isc[I_SUMV..] (all-reduced).
 void forward_half(topt_ctx* c, std::vector<Io>& io, bool want_adj, cudaStream_t st) {
@@ -642,6 +658,42 @@ void backward_half(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
   const bool leray = c->p.model == TOPT_INCOMPRESSIBLE;
   const double half = c->d == 3 ? 2.0 : 1.0;
   const double n_all = ntot(c);
+  if (merged_chain(c, io)) {
+    if (c->vf_pending) {
+      cudaStreamWaitEvent(st, c->ev_u, 0);
+      c->vf_pending = false;
+    } else {
+      vchain_fwd(c, io, st);
+    }
+    Slab& sl = c->slabs[0];
+    const double F8 = 8.0 * F, F16 = 16.0 * F, half = c->d == 3 ? 2.0 : 1.0;
+    float2* Z[4] = {sl.Z, sl.Z + F, sl.Z + 2 * F, sl.Z + 3 * F};
+    double2* Zv[3] = {sl.Zv, sl.Zv + F, sl.Zv + 2 * F};
+    int npz = 0;
+    {
+      const double bytes = d * F4 + half * F8 + (c->d == 3 ? 2 * half * F8 : 0.0) +       // b x, y forward
+                           half * (F16 + F8) + 2 * half * F8 +                                 // merged last axis
+                           (c->d == 3 ? 2 * 2 * half * F8 : 0.0);                            // y^-1 of g^, p^
+      Prof pr(c, K_BCHAIN, bytes, c->d == 3 ? 4 : 2, st);
+      bchain_xy(sl.g, sl.b, Z, false, st);
+      gchain_last(sl.g, Zv, Z, c->p.alpha, c->p.reg_order, (double)F, sl.partials, &npz, st);
+      gchain_yinv(sl.g, Z, st);
+    }
+    int np = 0;
+    {
+      Prof pr(c, K_ASSEMBLE, 2 * half * F8 + d * F4 + 2 * d * F4, 1, st);
+      launch_assemble(sl.g, sl.Z, true, nullptr, nullptr, io[0].v, io[0].isc + I_SUMV, io[0].g, io[0].s,
+                      sl.partials, &np, st, (double)F);
+    }
+    {
+      Prof pr(c, K_MISC, 0.0, 1, st);
+      launch_finalize_slots(sl.partials, 0, 10, np, true, io[0].isc + I_GMAX, st);
+      // v.u and s.u from the merged pass (slots 10, 11), unnormalised spectra: / n
+      launch_finalize_multi_k(sl.partials, 10, 2, npz, 1.0 / (double)F, io[0].isc + I_VU, st);
+    }
+    launch_finish(io[0].isc, io[0].scal, c->d, (double)F, c->cellvol, st);
+    return;
+  }
   // v-chain: u = alpha L v (fp64) when not supplied (or already running on the side stream)
   if (c->u_pending) {
     cudaStreamWaitEvent(st, c->ev_u, 0);
@@ -705,7 +757,7 @@ void backward_half(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
 // shared memory and leave most of the HBM bandwidth idle.  With z-slabs (NCCL exchanges
 // inside both) everything stays on `st`.
 topt_status eval_gradient(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
-  c->div_pending = c->u_pending = false;
+  c->div_pending = c->u_pending = c->vf_pending = false;
   // (profiling mode serialises everything on `st`, so the per-class times are standalone)
   if (P_of(c) == 1 && c->side && io[0].u == nullptr && !c->prof) {
     cudaEventRecord(c->ev_fork, st);
@@ -718,10 +770,15 @@ topt_status eval_gradient(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
       cudaEventRecord(c->ev_div, c->side);
       c->div_pending = true;
     }
-    run_vchain(c, io, c->side);
-    for (auto& x : io) x.u = nullptr;  // set again when the v-chain is joined
+    if (merged_chain(c, io)) {  // only the fp64 forward passes of v are independent of b
+      vchain_fwd(c, io, c->side);
+      c->vf_pending = true;
+    } else {
+      run_vchain(c, io, c->side);
+      for (auto& x : io) x.u = nullptr;  // set again when the v-chain is joined
+      c->u_pending = true;
+    }
     cudaEventRecord(c->ev_u, c->side);
-    c->u_pending = true;
   }
   forward_half(c, io, true, st);
   backward_half(c, io, st);
@@ -1409,8 +1466,10 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
   double te = now();
   {
     std::vector<Io> io = io_at(Vc, nullptr, Gc, Sc, 0);
+    c->want_u = true;  // the old chain: u = alpha L v^0 is carried from here on
     forward_half(c, io, true, st);
     backward_half(c, io, st);  // computes u = alpha L v^0 into utmp
+    c->want_u = false;
     for (auto& sl : c->slabs) cudaMemcpyAsync(sl.ucur, sl.utmp, V * 4, cudaMemcpyDeviceToDevice, st);
     TOPT_CHECK_LAUNCH();
   }

@@ -80,6 +80,8 @@ struct topt_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_div = nullptr, ev_u = nullptr;
   bool div_pending = false, u_pending = false;
+  bool vf_pending = false;  // side stream produces the fp64 forward v spectra (merged chain)
+  bool want_u = false;      // the caller needs u = alpha L v in utmp (solver start): old chain
   // streaming host-buffer evaluations (topt_eval_gradient_host_async): two staging slots
   cudaStream_t h_in = nullptr, h_comp = nullptr, h_out = nullptr;
   cudaEvent_t ev_hfork = nullptr, ev_hin[2]{}, ev_hfree[2]{}, ev_hdone[2]{}, ev_hout[2]{};

@@ -108,6 +108,11 @@ void bchain_xy(const Geom& g, const float* b, float2* const* Z, bool leray, cuda
 void bchain_last(const Geom& gz, float2* const* Z, double alpha, int p, bool leray, double n_total,
                  cudaStream_t st);
 void bchain_yinv(const Geom& g, float2* const* Z, bool leray, cudaStream_t st);
+// merged chain (non-Leray): fp64 v spectra + fp32 b spectra -> g^, p^ (fp32), y^-1 of both
+// (partial slots 10, 11: sum_x v.u and sum_x s.u by Parseval, *nparts blocks)
+void gchain_last(const Geom& gz, double2* const* Zv, float2* const* Zb, double alpha, int p, double n_total,
+                 double* partials, int* nparts, cudaStream_t st);
+void gchain_yinv(const Geom& g, float2* const* Z, cudaStream_t st);
 // x^-1 of the b-chain and pointwise assembly g = u + b_L, s = -(v - vbar) + p, with
 // partial sums in slots 0..9 (max|g|, sum gs, sum vu, sum su, sum g_c (3), sum s_c (3)).
 void launch_assemble(const Geom& g, const float2* Zb, bool leray, const float* b, const float* u, const float* v,
@@ -125,6 +130,8 @@ void launch_finalize_multi(const double* partials, int slot0, int nslots, int np
                            double* dst, cudaStream_t st);
 void launch_combine_obj(double* scalars, cudaStream_t st);  // OBJ = DIST + REG
 void launch_flag_to_double(const int* f, double* d, cudaStream_t st);
+void launch_finalize_multi_k(const double* partials, int first, int count, int nparts, double scale, double* dst,
+                             cudaStream_t st);
 // finalize slots [first, first+count) (slot 0 of the assembly = max) into dst
 void launch_finalize_slots(const double* partials, int first, int count, int nparts, bool first_is_max,
                            double* dst, cudaStream_t st);

@@ -651,6 +651,123 @@ __global__ void __launch_bounds__(kThreads, (MODE >= 4 ? 1 : 2)) k_rstrided(Geom
   }
 }
 
+// Merged last-axis pass of the v- and b-chains (non-Leray): the forward transform of the
+// v spectrum stays fp64 (the only place where rounding is amplified by alpha |k|^{2p},
+// DESIGN.md §6.3); at each k the fp64 product alpha L(k) v^ is added to the b spectrum and
+// the sum g^ = alpha L v^ + b^ and p^ = -b^/(alpha L~) are transformed back in fp32 — the
+// inverse passes of the fp64 chain and the separate u / b reads of the assembly disappear.
+// Field f of a tile: Zv[f] (fp64 (v_x + i v_y) | (v_z)), Zb[f] (fp32, same packing) ->
+// G[f] = Zb[f] (g packed alike), Pp[f] (p packed alike).  Radix 8 for both precisions.
+// u = alpha L v is never formed in space, so the sums the scalars need from it come from
+// Parseval on the unnormalised 3D spectra (packed pairs of real fields add their |.|^2
+// because the odd cross terms cancel under an even weight):
+//   sum_x v.u = (1/n) sum_k alpha L |V^|^2                      -> partial slot 10
+//   sum_x s.u = -(1/n) sum_k [alpha L |V^|^2 + Re(B^* V^)]_{k!=0} -> partial slot 11
+// (s = -(v - vbar) + p, sum u = 0, p^ = -B^/(alpha L~)).
+#ifndef TOPT_RZ_MINB
+#define TOPT_RZ_MINB 2
+#endif
+template <int N>
+__global__ void __launch_bounds__(kThreads, TOPT_RZ_MINB) k_rzmerge(Geom g, int axis, int TXC, ZList<double2> Zv,
+                                                         ZList<float2> Zb, ZList<float2> Pp, SpecOp op, int nitems,
+                                                         double* __restrict__ partials) {
+  double sumVU = 0.0, sumSU = 0.0;
+  constexpr int E = Ev<N, 8>::v, T = N / E;
+  using R = RfCfg<N, E>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int c = threadIdx.x % TXC, t = threadIdx.x / TXC;
+  double2* lbd = reinterpret_cast<double2*>(smraw) + c * R::STRIDE;  // fp64 line scratch
+  float2* lbf = reinterpret_cast<float2*>(smraw) + c * R::STRIDE;    // fp32 (same region, used after)
+  double2 twd[R::NTW];
+  float2 twf[R::NTW];
+  rf_twiddles<N, E>(twd, t);
+  rf_twiddles<N, E>(twf, t);
+  const int tilesx = g.nx / TXC;
+  const int outerN = axis == 1 ? g.nz : g.ny;
+  const int tiles = tilesx * outerN;
+  const unsigned Su = axis == 1 ? (unsigned)g.nx : (unsigned)g.nx * g.ny;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int tt = item % tiles, f = item / tiles;
+    const int x0 = (tt % tilesx) * TXC, outer = tt / tilesx;
+    const unsigned base = (axis == 1 ? ((unsigned)outer << (g.lx + g.ly)) : ((unsigned)outer << g.lx)) + x0 + c;
+    const int qx = x0 + c;
+    const double kx = qx <= g.nx / 2 ? qx : qx - g.nx;
+    double ky = 0.0;
+    if (g.d == 3) {
+      const int nyg = g.nyg ? g.nyg : g.ny;
+      const int qy = outer + g.ky0;
+      ky = qy <= nyg / 2 ? qy : qy - nyg;
+    }
+    double2 av[E];
+    float2 ab[E];
+    const double2* sv = Zv.z[f];
+    const float2* sb = Zb.z[f];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      av[e] = sv[base + (t + T * e) * Su];
+      ab[e] = sb[base + (t + T * e) * Su];
+    }
+    rf_fft<N, E, false, false>(av, lbd, t, twd);
+    rf_fft<N, E, false, false>(ab, lbf, t, twf);
+    float2 gg[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int q = t + T * e;
+      const double kq = q <= N / 2 ? q : q - N;
+      const double kk = g.d == 3 ? kx * kx + ky * ky + kq * kq : kx * kx + kq * kq;
+      const double Lk = regL(kk, op.p);
+      const double Lt = Lk == 0.0 ? 1.0 : Lk;  // kernel fix
+      const double mu = op.alpha * Lk * op.invn;
+      const double v2 = av[e].x * av[e].x + av[e].y * av[e].y;
+      sumVU += op.alpha * Lk * v2;
+      if (kk != 0.0) sumSU -= op.alpha * Lk * v2 + av[e].x * (double)ab[e].x + av[e].y * (double)ab[e].y;
+      gg[e] = make_float2((float)(mu * av[e].x + op.invn * (double)ab[e].x),
+                          (float)(mu * av[e].y + op.invn * (double)ab[e].y));
+      const float mp = -(float)op.invn * __frcp_rn((float)(op.alpha * Lt));
+      ab[e] = make_float2(ab[e].x * mp, ab[e].y * mp);
+    }
+    rf_fft<N, E, true, false>(gg, lbf, t, twf);
+    rf_fft<N, E, true, false>(ab, lbf, t, twf);
+    float2* dg = Zb.z[f];
+    float2* dp = Pp.z[f];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      dg[base + (t + T * e) * Su] = gg[e];
+      dp[base + (t + T * e) * Su] = ab[e];
+    }
+  }
+  // block tree reduction (blockDim is a power of two, possibly < 32 at small N)
+  __shared__ double red[2][kThreads];
+  red[0][threadIdx.x] = sumVU;
+  red[1][threadIdx.x] = sumSU;
+  __syncthreads();
+  for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+    if ((int)threadIdx.x < h) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + h];
+      red[1][threadIdx.x] += red[1][threadIdx.x + h];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < 2) partials[(size_t)(10 + threadIdx.x) * kMaxPartials + blockIdx.x] = red[threadIdx.x][0];
+}
+
+template <int N>
+static void rzmerge_launch(const Geom& g, int axis, const ZList<double2>& Zv, const ZList<float2>& Zb,
+                           const ZList<float2>& Pp, int nf, const SpecOp& op, double* partials, int* nparts,
+                           cudaStream_t st) {
+  constexpr int E = Ev<N, 8>::v, T = N / E;
+  int TXC = kThreads / T;
+  if (TXC > g.nx) TXC = g.nx;
+  const int threads = TXC * T;
+  const size_t sm = (size_t)TXC * RfCfg<N, E>::STRIDE * sizeof(double2);
+  const int outer = axis == 1 ? g.nz : g.ny;
+  const long long items = (long long)(g.nx / TXC) * outer * nf;
+  const int blocks = persistent_blocks(k_rzmerge<N>, threads, sm, items);
+  *nparts = blocks;
+  k_rzmerge<N><<<blocks, threads, sm, st>>>(g, axis, TXC, Zv, Zb, Pp, op, (int)items, partials);
+  count_launch();
+}
+
 // Assembly (x^-1 of the b-chain + pointwise combine), per x row (R9):
 //   g = u + b_L,  s = -(v - vbar) + p,  partial sums for the scalars.
 // Fields per row: non-Leray (p_x + i p_y)[, (p_z)], b_L = b from memory;
@@ -667,8 +784,11 @@ struct AsmArgs {
   double ntot;         // global point count (vbar = vsum / ntot)
 };
 
+#ifndef TOPT_ASM_MINB
+#define TOPT_ASM_MINB 2
+#endif
 template <int N, int LPR, bool LERAY>
-__global__ void __launch_bounds__(kThreads) k_rassemble(Geom g, AsmArgs a, int ngroups) {
+__global__ void __launch_bounds__(kThreads, TOPT_ASM_MINB) k_rassemble(Geom g, AsmArgs a, int ngroups) {
   constexpr int E = Ev<N, (LPR >= 4 ? 8 : 16)>::v, T = N / E, LPB = kThreads / T;
   constexpr bool WARP = T <= 32;
   using R = RfCfg<N, E, true>;
@@ -877,6 +997,26 @@ void bchain_last(const Geom& gz, float2* const* Z, double alpha, int p, bool ler
   } else {
     TOPT_DISPATCH_N2(Nl, (rstrided_launch<N_, kE32, 3, float2>(gz, axis, L, nin, nout, op, st)));
   }
+}
+
+// Merged last-axis pass (non-Leray): Zv (fp64 v spectra after x, y) and Zb (fp32 b
+// spectra after x, y) -> Zb = g^ (fp32), Zb[half + f] = p^; then the y^-1 pass of all four
+// (3D) / two (2D) fields, ready for the Leray-layout assembly with u = b = null.
+void gchain_last(const Geom& gz, double2* const* Zv, float2* const* Zb, double alpha, int p, double n_total,
+                 double* partials, int* nparts, cudaStream_t st) {
+  const int half = gz.d == 3 ? 2 : 1;
+  ZList<double2> V{{Zv[0], Zv[1], nullptr, nullptr}};
+  ZList<float2> B{{Zb[0], Zb[1], nullptr, nullptr}};
+  ZList<float2> Pp{{Zb[half], half > 1 ? Zb[half + 1] : nullptr, nullptr, nullptr}};
+  SpecOp op{alpha, p, 1.0 / n_total};
+  const int axis = gz.d == 3 ? 2 : 1, Nl = gz.d == 3 ? gz.nz : gz.ny;
+  TOPT_DISPATCH_N2(Nl, (rzmerge_launch<N_>(gz, axis, V, B, Pp, half, op, partials, nparts, st)));
+}
+void gchain_yinv(const Geom& g, float2* const* Z, cudaStream_t st) {
+  if (g.d != 3) return;
+  ZList<float2> L{{Z[0], Z[1], Z[2], Z[3]}};
+  SpecOp op{0.0, 1, 1.0};
+  TOPT_DISPATCH_N2(g.ny, (rstrided_launch<N_, kE32, 1, float2>(g, 1, L, 4, 4, op, st)));
 }
 
 // y^-1 pass of the b-chain (3D); the x^-1 pass is fused into the assembly.

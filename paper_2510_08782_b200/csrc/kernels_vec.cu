@@ -66,6 +66,13 @@ __global__ void k_finalize_slots(const double* __restrict__ partials, int nparts
   if (threadIdx.x == 0) dst[blockIdx.x] = sh[0];
 }
 
+// dst[i] = scale * sum of slot (first + i) (slots kMaxPartials apart), i < count
+void launch_finalize_multi_k(const double* partials, int first, int count, int nparts, double scale, double* dst,
+                             cudaStream_t st) {
+  k_finalize<<<count, 1024, 0, st>>>(partials + (size_t)first * kMaxPartials, nparts, scale, 0, dst, kMaxPartials);
+  count_launch();
+}
+
 void launch_finalize_slots(const double* partials, int first, int count, int nparts, bool first_is_max,
                            double* dst, cudaStream_t st) {
   k_finalize_slots<<<count, 1024, 0, st>>>(partials + (size_t)first * kMaxPartials, nparts, first_is_max ? 1 : 0, dst);

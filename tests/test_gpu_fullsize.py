@@ -123,11 +123,13 @@ def test_gradient_and_preconditioner_sampled_modes(run):
     assert np.linalg.norm(gh - gref) / np.linalg.norm(gref) < TOL
     assert np.linalg.norm(sh - sref) / np.linalg.norm(sref) < TOL
     # High |k| alone: there alpha L v dominates g and is the fp32 rounding noise of v amplified
-    # by alpha |k|^4 (an fp32 alpha L chain fails here).  Each mode of the fp32
-    # output g carries its own rounding noise, ~2^-24 rms(g) sqrt(N) per coefficient (4 sigma).
+    # by alpha |k|^4.  A forward transform of v in fp32 is off by O(1) at these modes (its
+    # rounding is amplified the same way); the fp64 forward transform is exact
+    # to the fp32 inverse passes, whose error per coefficient is ~ eps_32 log2(n) rms(g) sqrt(N)
+    # (bounded here with a factor 4), plus 1e-3 of the mode.
     hi = [i for i, k in enumerate(ks) if sum(x * x for x in k) > 64 ** 2]
-    noise = 4 * 2.0 ** -24 * np.sqrt(np.mean(run["g"] ** 2)) * np.sqrt(grid.npts)
-    assert np.all(np.abs(gh[hi] - gref[hi]) <= noise + TOL * np.abs(gref[hi]))
+    noise = 4 * np.log2(grid.npts) * 2.0 ** -24 * np.sqrt(np.mean(run["g"] ** 2)) * np.sqrt(grid.npts)
+    assert np.all(np.abs(gh[hi] - gref[hi]) <= noise + 1e-3 * np.abs(gref[hi]))
 
 
 def test_scalars(run):
