@@ -12,7 +12,7 @@
  *
  * Conventions (every entry point)
  *  - Grid: Omega = [0, 2pi)^d, d in {2, 3}, n[i] cells along x_{i+1}, h_i = 2pi/n[i]
- *    (P:126-134).  Each n[i] must be a power of two in [4, 1024] (TOPT_ERR_UNSUPPORTED
+ *    (P:126-134).  Each n[i] must be a power of two in [8, 1024] (TOPT_ERR_UNSUPPORTED
  *    otherwise); for d == 2, n[2] must be 1.
  *  - Fields are fp32, C order [n[2]][n[1]][n[0]] (x fastest), DEVICE pointers unless
  *    an entry point's name ends in _host.  A vector field is d consecutive scalar
