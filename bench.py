@@ -308,6 +308,20 @@ def run_topt(args):
         except Exception:
             traffic = None
     per_launch_bytes = dom["bytes"] / max(1, dom["launches"])
+    # The SL kernels are bound by shared-memory bandwidth, not HBM: a tricubic
+    # point reads 64 taps x 4 B from shared memory.  Peak = 148 SMs x 128 B/clk x the SM clock
+    # measured during the timed region (B300_MICROARCH.md: 128/N B/cyc/SM crossbar).
+    smem_roofline = None
+    sl = next((x for x in kern if x["name"] == "sl_step"), None)
+    if sl and sl["ms"] > 0:
+        taps_bytes = 64 * 4.0 * npts * sl["launches"]
+        sm_mhz = (clk.summary() or {}).get("sm_mhz") or 1965.0
+        nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+        speak = nsm * 128.0 * sm_mhz * 1e6 / 1e9
+        sach = taps_bytes / (sl["ms"] / 1e3) / 1e9
+        smem_roofline = {"kernel": "sl_step", "bound": "smem", "achieved": round(sach, 1), "peak": round(speak, 1),
+                         "unit": "GB/s", "frac": round(sach / speak, 4),
+                         "bytes_per_point": 256, "peak_kind": f"derived: {nsm} SMs x 128 B/clk x {sm_mhz:.0f} MHz"}
     roofline = {"bound": "hbm", "kernel": dom["name"], "achieved": round(achieved, 1), "peak": peak,
                 "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                 "algorithmic_bytes_per_launch": per_launch_bytes, "peak_kind": peak_kind,
@@ -405,6 +419,7 @@ def run_topt(args):
             "e2e": e2e,
             "gpu_launches": launches,
             "roofline": roofline,
+            "smem_roofline": smem_roofline,
             "cpu_baseline": cpu,
             "hbm_frac_pass_model": round(model_bytes * (value if slab else value / world) / (peak * 1e9), 4),
             "pass_model_bytes_per_eval": model_bytes,
