@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("model", [0, 1, 2])
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", [2, 4, 8])
 def test_eval_gradient_slab_invariance(model, P):
     d = case(2, (64, 32, 32), model=model)
     if model == 2:
@@ -42,7 +42,7 @@ def test_objective_slab_invariance():
         assert abs(o1[k] - o4[k]) <= 1e-6 * abs(o1[k]), k
 
 
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", [2, 8])
 def test_solve_slab_invariance(P):
     """20 GA-NGMRES iterations on P emulated slabs vs one slab (replayed step sequence)."""
     d = case(2, (64, 32, 32))
