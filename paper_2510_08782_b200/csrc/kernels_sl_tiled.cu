@@ -11,11 +11,12 @@
 // halo fall back to the L1 gather for that point (correct for any CFL).
 //
 // Single-field kernels (SL step, last step, Heun factor): k_sl_pipe, a cp.async pipeline.
-//   * the ring has NZR = 2H + 2K = 16 slots (slot = plane & 15); the K planes of stage i+2
+//   * the ring has NZR = 2H + 2K = 16 slots (slot = plane & 15); the K planes of stage i+1
 //     are copied global -> shared with cp.async (no register staging, no loader role)
-//     while stage i is computed, so HBM latency is covered by 2 stages of K planes;
-//   * per stage: one wait + barrier before the K planes are computed, one barrier before
-//     their oldest slots are refilled — 2 barriers per K = 4 planes;
+//     while stage i is computed;
+//   * ONE barrier per stage (TOPT_SL_ONEBAR): after it every thread has finished stage
+//     i-1, whose oldest K slots are refilled with stage i+1's planes (prefetch distance one
+//     stage of K = 4 planes, NZR >= 2H + 2K) — half the barriers of a wait/refill pair;
 //   * the per-point streams (delta, E) are prefetched into registers one plane ahead.
 // Trace (3 fields, RK2 midpoint feet): k_sl_trace, ring of 2H+2 slots with one plane
 // prefetched into registers (H = 2: the midpoint displacement dt/2 v has |floor| <= 1).
@@ -149,6 +150,9 @@ constexpr int NF4 = PH * (tiled::XW / 4);  // float4 per plane
 constexpr size_t SMEM = (size_t)NZR * PS * sizeof(float);
 }  // namespace pipe
 
+#ifndef TOPT_SL_ONEBAR
+#define TOPT_SL_ONEBAR 1  // one block barrier per K-plane stage (prefetch distance 1 stage)
+#endif
 #ifndef TOPT_SL_MINB
 #define TOPT_SL_MINB 3  // resident blocks per SM the register budget is sized for
 #endif
@@ -208,30 +212,46 @@ __global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, T
   const int nst = ZC / K;
   load_planes(z0 - H, z0 + K + H);  // stage 0
   cp_commit();
+#if !TOPT_SL_ONEBAR
   if (nst > 1) load_stage(z0 + K + H);  // stage 1
   cp_commit();
+#endif
 
   const size_t gi0 = (size_t)z0 * plane + (size_t)(y0 + ty) * g.nx + x0 + tx;
+  // per-thread stream bases; offsets from them fit 32 bits (3F < 2^32 for every supported grid)
+  const float* __restrict__ pd = a.delta + gi0;
+  const float* __restrict__ pE = HAS_E ? a.E + gi0 : nullptr;
+  float* __restrict__ pout = a.out[0] + gi0;
+  const unsigned F32 = (unsigned)F, P32 = (unsigned)plane;
   // per-point streams (delta_x, delta_y, delta_z, E), prefetched one plane ahead
   float n0, n1, n2, nE = 1.0f;
   auto fetch = [&](int zi) {
-    const size_t gi = gi0 + (size_t)zi * plane;
-    n0 = __ldg(a.delta + gi);
-    n1 = __ldg(a.delta + F + gi);
-    n2 = __ldg(a.delta + 2 * F + gi);
-    if (HAS_E) nE = __ldg(a.E + gi);
+    const unsigned o = (unsigned)zi * P32;
+    n0 = __ldg(pd + o);
+    n1 = __ldg(pd + (F32 + o));
+    n2 = __ldg(pd + (2u * F32 + o));
+    if (HAS_E) nE = __ldg(pE + o);
   };
   fetch(0);
   double acc = 0.0;
 
 #pragma unroll 1
   for (int st = 0; st < nst; ++st) {
+#if TOPT_SL_ONEBAR
+    // one barrier per stage: after it every thread has finished stage st-1, whose oldest
+    // K slots (planes needed by no later stage, NZR >= 2H + 2K) take stage st+1's planes
+    cp_wait<0>();
+    __syncthreads();
+    if (st + 1 < nst) load_stage(z0 + (st + 1) * K + H);
+    cp_commit();
+#else
     cp_wait<1>();  // this stage's planes have landed (the next stage's may be in flight)
     __syncthreads();
+#endif
 #pragma unroll 1
     for (int j = 0; j < K; ++j) {
       const int zi = st * K + j, z = z0 + zi;
-      const size_t gi = gi0 + (size_t)zi * plane;
+      const unsigned o = (unsigned)zi * P32;
       const float dx = n0, dy = n1, dz = n2, cE = nE;
       if (zi + 1 < ZC) fetch(zi + 1);
       const float fx = floorf(dx), fy = floorf(dy), fz = floorf(dz);
@@ -250,21 +270,24 @@ __global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, T
       }
       if (MODE == M_EFACTOR) {
         const float bv = sm[(z & (NZR - 1)) * PS + (ty + H) * PW + tx + XH];  // divv(l)
-        a.out[0][gi] = 1.0f + a.sh * (r + bv) + a.h2 * r * bv;
+        pout[o] = 1.0f + a.sh * (r + bv) + a.h2 * r * bv;
       } else {
         float val = r;
         if (HAS_E) val *= cE;
-        a.out[0][gi] = val;
+        pout[o] = val;
         if (MODE == M_LAST) {
+          const size_t gi = gi0 + o;
           const float res = __ldg(a.m1 + gi) - val;
           if (a.lamS) a.lamS[gi] = res;
           acc += (double)res * (double)res;
         }
       }
     }
+#if !TOPT_SL_ONEBAR
     __syncthreads();  // every thread is done with the oldest K slots
     if (st + 2 < nst) load_stage(z0 + (st + 2) * K + H);
     cp_commit();
+#endif
   }
   cp_wait<0>();
 
