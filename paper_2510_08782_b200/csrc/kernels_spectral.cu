@@ -664,6 +664,9 @@ __global__ void __launch_bounds__(kThreads, (MODE >= 4 ? 1 : 2)) k_rstrided(Geom
 //   sum_x v.u = (1/n) sum_k alpha L |V^|^2                      -> partial slot 10
 //   sum_x s.u = -(1/n) sum_k [alpha L |V^|^2 + Re(B^* V^)]_{k!=0} -> partial slot 11
 // (s = -(v - vbar) + p, sum u = 0, p^ = -B^/(alpha L~)).
+#ifndef TOPT_RZ_PF
+#define TOPT_RZ_PF 1  // merged last-axis pass: cp.async staging of the next item's lines
+#endif
 #ifndef TOPT_RZ_MINB
 #define TOPT_RZ_MINB 2
 #endif
@@ -686,6 +689,30 @@ __global__ void __launch_bounds__(kThreads, TOPT_RZ_MINB) k_rzmerge(Geom g, int 
   const int outerN = axis == 1 ? g.nz : g.ny;
   const int tiles = tilesx * outerN;
   const unsigned Su = axis == 1 ? (unsigned)g.nx : (unsigned)g.nx * g.ny;
+#if TOPT_RZ_PF
+  // staging tiles [N rows][TXC columns] of the fp64 v and fp32 b lines of the NEXT item,
+  // filled with cp.async (16-byte chunks: one double2, or two float2) while this item's
+  // lines are transformed, so the strided HBM reads overlap the fp64 FFT work
+  double2* Sv = reinterpret_cast<double2*>(smraw) + TXC * R::STRIDE;
+  float2* Sb = reinterpret_cast<float2*>(Sv + N * TXC);
+  auto stage = [&](int it) {
+    const int tt = it % tiles, f = it / tiles;
+    const int x0 = (tt % tilesx) * TXC, outer = tt / tilesx;
+    const unsigned t0 = (axis == 1 ? ((unsigned)outer << (g.lx + g.ly)) : ((unsigned)outer << g.lx)) + x0;
+    const double2* sv = Zv.z[f];
+    const float2* sb = Zb.z[f];
+    for (int i = threadIdx.x; i < N * TXC; i += blockDim.x) {
+      const int row = i / TXC, k = i % TXC;
+      cp_async16_f(Sv + row * TXC + k, reinterpret_cast<const float*>(sv + t0 + row * Su + k));
+    }
+    for (int i = threadIdx.x; i < N * TXC / 2; i += blockDim.x) {
+      const int row = i / (TXC / 2), k = i % (TXC / 2);
+      cp_async16_f(Sb + row * TXC + 2 * k, reinterpret_cast<const float*>(sb + t0 + row * Su + 2 * k));
+    }
+  };
+  if ((int)blockIdx.x < nitems) stage(blockIdx.x);
+  cp_commit_f();
+#endif
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
     const int tt = item % tiles, f = item / tiles;
     const int x0 = (tt % tilesx) * TXC, outer = tt / tilesx;
@@ -700,6 +727,20 @@ __global__ void __launch_bounds__(kThreads, TOPT_RZ_MINB) k_rzmerge(Geom g, int 
     }
     double2 av[E];
     float2 ab[E];
+#if TOPT_RZ_PF
+    // this item's lines were staged by the previous iteration (or the prologue); take them,
+    // free the staging tiles and start the next item's copies before the transforms
+    cp_wait0_f();
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      av[e] = Sv[(t + T * e) * TXC + c];
+      ab[e] = Sb[(t + T * e) * TXC + c];
+    }
+    __syncthreads();
+    if (item + (int)gridDim.x < nitems) stage(item + gridDim.x);
+    cp_commit_f();
+#else
     const double2* sv = Zv.z[f];
     const float2* sb = Zb.z[f];
 #pragma unroll
@@ -707,6 +748,7 @@ __global__ void __launch_bounds__(kThreads, TOPT_RZ_MINB) k_rzmerge(Geom g, int 
       av[e] = sv[base + (t + T * e) * Su];
       ab[e] = sb[base + (t + T * e) * Su];
     }
+#endif
     rf_fft<N, E, false, false>(av, lbd, t, twd);
     rf_fft<N, E, false, false>(ab, lbf, t, twf);
     float2 gg[E];
@@ -759,7 +801,8 @@ static void rzmerge_launch(const Geom& g, int axis, const ZList<double2>& Zv, co
   int TXC = kThreads / T;
   if (TXC > g.nx) TXC = g.nx;
   const int threads = TXC * T;
-  const size_t sm = (size_t)TXC * RfCfg<N, E>::STRIDE * sizeof(double2);
+  size_t sm = (size_t)TXC * RfCfg<N, E>::STRIDE * sizeof(double2);
+  if (TOPT_RZ_PF) sm += (size_t)N * TXC * (sizeof(double2) + sizeof(float2));  // staging tiles
   const int outer = axis == 1 ? g.nz : g.ny;
   const long long items = (long long)(g.nx / TXC) * outer * nf;
   const int blocks = persistent_blocks(k_rzmerge<N>, threads, sm, items);
