@@ -161,6 +161,9 @@ constexpr size_t SMEM = (size_t)NZR * PS * sizeof(float);
 #ifndef TOPT_SL_ONEBAR
 #define TOPT_SL_ONEBAR 1  // one block barrier per K-plane stage (prefetch distance 1 stage)
 #endif
+#ifndef TOPT_SL_XWIN
+#define TOPT_SL_XWIN 1  // warp-uniform 5-column x window when the warp's x floors span two values
+#endif
 #ifndef TOPT_SL_MINB
 #define TOPT_SL_MINB 3  // resident blocks per SM the register budget is sized for
 #endif
@@ -270,7 +273,50 @@ __global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, T
       const float fx = floorf(dx), fy = floorf(dy), fz = floorf(dz);
       const int ix = (int)fx, iy = (int)fy, iz = (int)fz;
       float r;
-      if (ix < -XH + 1 || ix > XH - 2 || iy < -H + 1 || iy > H - 2 || iz < -H + 1 || iz > H - 2) {
+      const bool inr = !(ix < -XH + 1 || ix > XH - 2 || iy < -H + 1 || iy > H - 2 || iz < -H + 1 || iz > H - 2);
+#if TOPT_SL_XWIN
+      // x-window path (warp-uniform): when the warp's x floors take exactly two values
+      // {mn, mn+1}, the 32 lanes' 4-tap x stencils span 33 columns and EVERY tap of the
+      // per-lane path costs two smem wavefronts (columns c and c+32 share a bank).  Instead each
+      // lane reads the 5 columns mn-1 .. mn+3 relative to its own x — the same offsets in
+      // every lane, so each load is one conflict-free wavefront whatever the lanes' rows and
+      // planes — with its 4 x weights at offset ix - mn of a 5-vector: 80 wavefronts per
+      // point instead of 128.  Contraction order x, then y, then z.
+      const int mn = __reduce_min_sync(0xffffffffu, ix), mx = __reduce_max_sync(0xffffffffu, ix);
+      if (mx == mn + 1 && __all_sync(0xffffffffu, inr)) {
+        float wx[4], wy[4], wz[4];
+        lag4(dx - fx, wx);
+        lag4(dy - fy, wy);
+        lag4(dz - fz, wz);
+        const bool sh = ix != mn;
+        float w5[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) w5[k] = sh ? (k > 0 ? wx[k - 1] : 0.0f) : (k < 4 ? wx[k] : 0.0f);
+        const int p0 = z + iz - 1;
+        const int ro = (ty + iy - 1 + H) * PW + tx + mn - 1 + XH;
+        const float* s0 = sm + ((p0) & (NZR - 1)) * PS + ro;
+        const float* s1 = sm + ((p0 + 1) & (NZR - 1)) * PS + ro;
+        const float* s2 = sm + ((p0 + 2) & (NZR - 1)) * PS + ro;
+        const float* s3 = sm + ((p0 + 3) & (NZR - 1)) * PS + ro;
+        float2 lo = make_float2(0.f, 0.f), hi = lo;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          float2 r01 = make_float2(0.f, 0.f), r23 = r01;
+#pragma unroll
+          for (int k = 0; k < 5; ++k) {
+            const int oo = b * PW + k;
+            const float2 w = make_float2(w5[k], w5[k]);
+            r01 = __ffma2_rn(w, make_float2(s0[oo], s1[oo]), r01);
+            r23 = __ffma2_rn(w, make_float2(s2[oo], s3[oo]), r23);
+          }
+          const float2 wb = make_float2(wy[b], wy[b]);
+          lo = __ffma2_rn(wb, r01, lo);
+          hi = __ffma2_rn(wb, r23, hi);
+        }
+        r = fmaf(wz[3], hi.y, fmaf(wz[2], hi.x, fmaf(wz[1], lo.y, wz[0] * lo.x)));
+      } else
+#endif
+      if (!inr) {
         r = gather_global(g, in, x0 + tx, y0 + ty, z, dx, dy, dz);
       } else {
         float wx[4], wy[4], wz[4];
