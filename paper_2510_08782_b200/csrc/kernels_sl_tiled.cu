@@ -161,6 +161,9 @@ constexpr size_t SMEM = (size_t)NZR * PS * sizeof(float);
 #ifndef TOPT_SL_ONEBAR
 #define TOPT_SL_ONEBAR 1  // one block barrier per K-plane stage (prefetch distance 1 stage)
 #endif
+#ifndef TOPT_TRACE2
+#define TOPT_TRACE2 1  // z-pair trace kernel (k_sl_trace2)
+#endif
 #ifndef TOPT_SL_XWIN
 #define TOPT_SL_XWIN 1  // warp-uniform 5-column x window when the warp's x floors span two values
 #endif
@@ -528,6 +531,186 @@ __global__ void __launch_bounds__(256, 2) k_sl_trace(Geom g, int ZC, TileArgs a)
   }
 }
 
+// =====================================================================================
+// Trace, z-pair form (k_sl_trace2): a thread computes the feet of the points (z, z+1) of its
+// column.  When every lane of the warp has |c/2| < 1 per axis for both points (c = dt v/h in
+// cells), the four stencils (2 points x 2 sides) lie in the FIXED window of nodes -2..2 in
+// x and y and planes z-2 .. z+3: each window row (5 consecutive words, the same offsets in
+// every lane: conflict-free) is loaded ONCE and contracted with both points' x weights
+// (forward/adjoint packed as fp32x2) — 150 smem loads per component per pair instead of
+// 250.  Otherwise the pair takes the per-point paths of k_sl_trace.  The 8-slot plane ring is
+// filled with cp.async, two planes per step, one barrier per pair.
+// =====================================================================================
+__global__ void __launch_bounds__(256, 2) k_sl_trace2(Geom g, int ZC, TileArgs a) {
+  using namespace tiled;
+  constexpr int HALO = 2, NF = 3, NZR = 8;
+  constexpr int PS = Cfg<HALO>::PS, PH = Cfg<HALO>::PH, NF4 = PH * (XW / 4);
+  extern __shared__ __align__(16) float sm[];  // [NF][NZR][PS]
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int tilesx = g.nx / TX, tilesy = g.ny / TY;
+  int bid = blockIdx.x;
+  const int bx = bid % tilesx;
+  bid /= tilesx;
+  const int by = bid % tilesy;
+  bid /= tilesy;
+  const int z0 = bid * ZC;
+  const int x0 = bx * TX, y0 = by * TY;
+  const size_t F = g.F;
+  const size_t plane = (size_t)g.nx * g.ny;
+  auto psrc = [&](int pl) -> size_t { return (size_t)(g.zh ? pl + g.zh : (pl & (g.nz - 1))) * plane; };
+  auto load_planes = [&](int pa, int pb) {  // planes [pa, pb) of the 3 components
+    const int n = (pb - pa) * NF * NF4;
+    for (int i = threadIdx.x; i < n; i += 256) {
+      const int pl = pa + i / (NF * NF4), rem = i % (NF * NF4), f = rem / NF4, q = rem % NF4;
+      const int r = q / (XW / 4), k = q % (XW / 4);
+      const size_t src = psrc(pl) + (size_t)((y0 - HALO + r) & (g.ny - 1)) * g.nx + ((x0 - XH + 4 * k) & (g.nx - 1));
+      cp_async16(sm + (f * NZR + (pl & (NZR - 1))) * PS + r * PW + 4 * k, a.in[f] + src);
+    }
+  };
+  load_planes(z0 - HALO, z0 + 2 + HALO);  // planes of the first pair
+  cp_commit();
+
+  double vs0 = 0.0, vs1 = 0.0, vs2 = 0.0;
+  const size_t gi0 = (size_t)z0 * plane + (size_t)(y0 + ty) * g.nx + x0 + tx;
+  const int rbase = (ty - 2 + HALO) * PW + tx - 2 + XH;
+  // (forward, adjoint) weights of one point on window nodes -2..2 per axis
+  auto weights = [&](const float cc[3], float2 (&W)[3][5]) {
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      const float dF = 0.5f * -1.0f * cc[ax], dA = 0.5f * 1.0f * cc[ax];
+      const float fF = floorf(dF), fA = floorf(dA);
+      float wF[4], wA[4];
+      lag4(dF - fF, wF);
+      lag4(dA - fA, wA);
+      const bool sF = fF == 0.0f, sA = fA == 0.0f;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const float f0 = k < 4 ? wF[k] : 0.0f, f1 = k > 0 ? wF[k - 1] : 0.0f;
+        const float a0 = k < 4 ? wA[k] : 0.0f, a1 = k > 0 ? wA[k - 1] : 0.0f;
+        W[ax][k] = make_float2(sF ? f1 : f0, sA ? a1 : a0);
+      }
+    }
+  };
+  // per-point, per-side path (k_sl_trace's): stencil at the foot's own floors
+  auto single = [&](int z, size_t gi, const float cc[3]) {
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      float* o = a.out[side];
+      if (!o) continue;
+      const float sg = side == 0 ? -1.0f : 1.0f;
+      const float dx = 0.5f * sg * cc[0], dy = 0.5f * sg * cc[1], dz = 0.5f * sg * cc[2];
+      const float fx = floorf(dx), fy = floorf(dy), fz = floorf(dz);
+      const int ix = (int)fx, iy = (int)fy, iz = (int)fz;
+      float r[NF];
+      if (ix < -XH + 1 || ix > XH - 2 || iy < -HALO + 1 || iy > HALO - 2 || iz < -HALO + 1 || iz > HALO - 2) {
+#pragma unroll
+        for (int f = 0; f < NF; ++f) r[f] = gather_global(g, a.in[f], x0 + tx, y0 + ty, z, dx, dy, dz);
+      } else {
+        float wx[4], wy[4], wz[4];
+        lag4(dx - fx, wx);
+        lag4(dy - fy, wy);
+        lag4(dz - fz, wz);
+        const int p0 = z + iz - 1;
+        gather_smem<NF, NZR * PS>(sm, [&](int c) { return ((p0 + c) & (NZR - 1)) * PS; },
+                                  (ty + iy - 1 + HALO) * PW + tx + ix - 1 + XH, wx, wy, wz, r);
+      }
+      o[gi] = sg * g.cx * r[0];
+      o[F + gi] = sg * g.cy * r[1];
+      o[2 * F + gi] = sg * g.cz * r[2];
+    }
+  };
+
+#pragma unroll 1
+  for (int zi = 0; zi < ZC; zi += 2) {
+    const int z = z0 + zi;
+    cp_wait<0>();
+    __syncthreads();  // planes z-2 .. z+3 resident; everyone is done with the previous pair
+    if (zi + 2 < ZC) load_planes(z + 2 + HALO, z + 4 + HALO);  // over planes z-4, z-3
+    cp_commit();
+    const size_t gA = gi0 + (size_t)zi * plane, gB = gA + plane;
+    const int cA = (z & (NZR - 1)) * PS + (ty + HALO) * PW + tx + XH;
+    const int cB = ((z + 1) & (NZR - 1)) * PS + (ty + HALO) * PW + tx + XH;
+    float ccA[3], ccB[3];
+    const float gc[3] = {g.cx, g.cy, g.cz};
+    bool ok = true;
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      const float uA = sm[f * NZR * PS + cA], uB = sm[f * NZR * PS + cB];
+      ccA[f] = uA * gc[f];
+      ccB[f] = uB * gc[f];
+      ok = ok && fabsf(ccA[f]) < 2.0f && fabsf(ccB[f]) < 2.0f;
+      if (f == 0) vs0 += (double)uA + (double)uB;
+      if (f == 1) vs1 += (double)uA + (double)uB;
+      if (f == 2) vs2 += (double)uA + (double)uB;
+    }
+    if (__all_sync(0xffffffffu, ok)) {
+      float2 WA[3][5], WB[3][5];
+      weights(ccA, WA);
+      weights(ccB, WB);
+#pragma unroll 1
+      for (int f = 0; f < NF; ++f) {
+        float2 resA = make_float2(0.f, 0.f), resB = resA;
+#pragma unroll
+        for (int cz = 0; cz < 6; ++cz) {  // window planes z-2 .. z+3
+          const float* pp = sm + (f * NZR + ((z - 2 + cz) & (NZR - 1))) * PS + rbase;
+          float2 plA = make_float2(0.f, 0.f), plB = plA;
+#pragma unroll
+          for (int yb = 0; yb < 5; ++yb) {
+            float sv[5];
+#pragma unroll
+            for (int k = 0; k < 5; ++k) sv[k] = pp[yb * PW + k];
+            if (cz < 5) {
+              float2 row = __fmul2_rn(WA[0][0], make_float2(sv[0], sv[0]));
+#pragma unroll
+              for (int k = 1; k < 5; ++k) row = __ffma2_rn(WA[0][k], make_float2(sv[k], sv[k]), row);
+              plA = __ffma2_rn(WA[1][yb], row, plA);
+            }
+            if (cz > 0) {
+              float2 row = __fmul2_rn(WB[0][0], make_float2(sv[0], sv[0]));
+#pragma unroll
+              for (int k = 1; k < 5; ++k) row = __ffma2_rn(WB[0][k], make_float2(sv[k], sv[k]), row);
+              plB = __ffma2_rn(WB[1][yb], row, plB);
+            }
+          }
+          if (cz < 5) resA = __ffma2_rn(WA[2][cz], plA, resA);
+          if (cz > 0) resB = __ffma2_rn(WB[2][cz - 1], plB, resB);
+        }
+        const float sc = f == 0 ? g.cx : (f == 1 ? g.cy : g.cz);
+        if (a.out[0]) {
+          a.out[0][f * F + gA] = -1.0f * sc * resA.x;
+          a.out[0][f * F + gB] = -1.0f * sc * resB.x;
+        }
+        if (a.out[1]) {
+          a.out[1][f * F + gA] = 1.0f * sc * resA.y;
+          a.out[1][f * F + gB] = 1.0f * sc * resB.y;
+        }
+      }
+    } else {
+      single(z, gA, ccA);
+      single(z + 1, gB, ccB);
+    }
+  }
+  cp_wait<0>();
+
+  if (a.partials) {
+    __shared__ double redv[3][8];
+    double v3[3] = {vs0, vs1, vs2};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double t = v3[c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+      if ((threadIdx.x & 31) == 0) redv[c][threadIdx.x >> 5] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+      double t = 0.0;
+      for (int w = 0; w < 8; ++w) t += redv[threadIdx.x][w];
+      a.partials[(size_t)threadIdx.x * kMaxPartials + blockIdx.x] = t;
+    }
+  }
+}
+
 // ---- host side ------------------------------------------------------------------------
 bool tiled_ok(const Geom& g) {
   return g.d == 3 && g.nx >= tiled::TX && g.nx % tiled::TX == 0 && g.ny % tiled::TY == 0 &&
@@ -588,12 +771,21 @@ void tiled_trace(const Geom& g, const float* v, float* df, float* da, double* vs
   for (int c = 0; c < 3; ++c) a.in[c] = v + c * cs;
   a.out[0] = df;
   a.out[1] = da;
+#if TOPT_TRACE2
+  const size_t sm = (size_t)3 * 8 * tiled::Cfg<HALO>::PS * sizeof(float);
+  static int resident = 0;
+  if (!resident) resident = resident_blocks(k_sl_trace2, 256, sm);
+  const int zc = tiled_zc(g, HALO, 2, resident);
+  const int blocks = (g.nx / tiled::TX) * (g.ny / tiled::TY) * (g.nz / zc);
+  k_sl_trace2<<<blocks, 256, sm, st>>>(g, zc, a);
+#else
   const size_t sm = (size_t)3 * (2 * HALO + 2) * tiled::Cfg<HALO>::PS * sizeof(float);
   static int resident = 0;
   if (!resident) resident = resident_blocks(k_sl_trace<HALO>, 256, sm);
   const int zc = tiled_zc(g, HALO, 1, resident);
   const int blocks = (g.nx / tiled::TX) * (g.ny / tiled::TY) * (g.nz / zc);
   k_sl_trace<HALO><<<blocks, 256, sm, st>>>(g, zc, a);
+#endif
   count_launch();
   if (nparts) *nparts = blocks;
 }
