@@ -241,6 +241,7 @@ def run_topt(args):
     torch.cuda.set_device(dev)
     n = tuple(args.n) if args.n else None
     d = make_problem(args.config, n, device=str(dev))
+    torch.cuda.empty_cache()  # the generator's device temporaries (512^3: ~100 GB cached)
     cfgp = dict(n=tuple(d["n"]), nt=d["nt"], model=d["model"], reg_order=d["reg_order"], alpha=d["alpha"])
     slab = world > 1 and args.parallel == "slab"
     if slab:  # one z-slab per GPU over NCCL
@@ -364,7 +365,10 @@ def run_topt(args):
     # mixing, stop test) on the same problem from v^0 = 0, after freeing the evaluation context
     solver = None
     if args.solver_iters > 0:
+        host_eval = None  # a bound method keeps the evaluation context (and its workspace) alive
         del t
+        import gc
+        gc.collect()
         torch.cuda.empty_cache()
         kw = dict(window=d["window"], sigma=d.get("sigma", 1), tau=d.get("tau", 0), max_iter=args.solver_iters,
                   eps_rel=0.0, **cfgp)

@@ -144,3 +144,24 @@ def test_forward_large_displacement_fallback():
     traj = host(t.forward(dev(d["m0"]), dev(d["v"])))
     _, _, _, ref = ogr.forward_solve(d["prob"], d["v"])
     assert rel_l2(traj[-1], ref[-1]) < TOL
+
+
+@pytest.mark.parametrize("scale", [1.5, 4.0])
+def test_feet_and_steps_mixed_kernel_paths(scale):
+    """Velocities large enough that, within one launch, some warps take the fixed-window paths
+    (trace: |dt v / 2h| < 1 in every lane; SL step: x floors spanning two values) and others the
+    per-point stencils or the L1 gather (|delta| > 3 cells): every path must match the oracle."""
+    d = case(2, (64, 32, 32), scale=scale)
+    rf, ra = transport.feet(d["grid"], d["v"], d["nt"])
+    half = 0.5 * np.max(np.abs(rf))
+    assert half > 1.0  # some midpoints leave the union window
+    t = topt_for(d)
+    df, da = t.feet(dev(d["v"]))
+    assert rel_l2(host(df), rf) < TOL
+    assert rel_l2(host(da), ra) < TOL
+    for model in (0, 1):
+        dm = case(2, (64, 32, 32), scale=scale, model=model)
+        tm = topt_for(dm)
+        traj = host(tm.forward(dev(dm["m0"]), dev(dm["v"])))
+        _, _, _, ref = ogr.forward_solve(dm["prob"], dm["v"])
+        assert rel_l2(traj[-1], ref[-1]) < TOL, model
