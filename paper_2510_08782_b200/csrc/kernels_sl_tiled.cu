@@ -14,7 +14,7 @@
 //   * the ring has NZR = 2H + 2K = 16 slots (slot = plane & 15); the K planes of stage i+1
 //     are copied global -> shared with cp.async (no register staging, no loader role)
 //     while stage i is computed;
-//   * ONE barrier per stage (TOPT_SL_ONEBAR): after it every thread has finished stage
+//   * ONE barrier per stage: after it every thread has finished stage
 //     i-1, whose oldest K slots are refilled with stage i+1's planes (prefetch distance one
 //     stage of K = 4 planes, NZR >= 2H + 2K) — half the barriers of a wait/refill pair;
 //   * the per-point streams (delta, E) are prefetched into registers one plane ahead.
@@ -158,9 +158,6 @@ constexpr int NF4 = PH * (tiled::XW / 4);  // float4 per plane
 constexpr size_t SMEM = (size_t)NZR * PS * sizeof(float);
 }  // namespace pipe
 
-#ifndef TOPT_SL_ONEBAR
-#define TOPT_SL_ONEBAR 1  // one block barrier per K-plane stage (prefetch distance 1 stage)
-#endif
 #ifndef TOPT_TRACE2
 #define TOPT_TRACE2 1  // z-pair trace kernel (k_sl_trace2)
 #endif
@@ -226,15 +223,10 @@ __global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, T
   const int nst = ZC / K;
   load_planes(z0 - H, z0 + K + H);  // stage 0
   cp_commit();
-#if TOPT_SL_ONEBAR
   for (int u = 1; u < pipe::D; ++u) {  // stages 1 .. D-1
     if (u < nst) load_stage(z0 + u * K + H);
     cp_commit();
   }
-#else
-  if (nst > 1) load_stage(z0 + K + H);  // stage 1
-  cp_commit();
-#endif
 
   const size_t gi0 = (size_t)z0 * plane + (size_t)(y0 + ty) * g.nx + x0 + tx;
   // per-thread stream bases; offsets from them fit 32 bits (3F < 2^32 for every supported grid)
@@ -256,17 +248,12 @@ __global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, T
 
 #pragma unroll 1
   for (int st = 0; st < nst; ++st) {
-#if TOPT_SL_ONEBAR
     // one barrier per stage: after it every thread has finished stage st-1, whose oldest
-    // K slots (planes needed by no later stage, NZR >= 2H + 2K) take stage st+1's planes
+    // K slots (planes needed by no later stage, NZR >= 2H + (D+1)K) take stage st+D's planes
     cp_wait<pipe::D - 1>();
     __syncthreads();
     if (st + pipe::D < nst) load_stage(z0 + (st + pipe::D) * K + H);
     cp_commit();
-#else
-    cp_wait<1>();  // this stage's planes have landed (the next stage's may be in flight)
-    __syncthreads();
-#endif
 #pragma unroll 1
     for (int j = 0; j < K; ++j) {
       const int zi = st * K + j, z = z0 + zi;
@@ -345,11 +332,6 @@ __global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, T
         }
       }
     }
-#if !TOPT_SL_ONEBAR
-    __syncthreads();  // every thread is done with the oldest K slots
-    if (st + 2 < nst) load_stage(z0 + (st + 2) * K + H);
-    cp_commit();
-#endif
   }
   cp_wait<0>();
 
