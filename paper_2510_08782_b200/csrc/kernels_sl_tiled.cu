@@ -18,8 +18,11 @@
 //     i-1, whose oldest K slots are refilled with stage i+1's planes (prefetch distance one
 //     stage of K = 4 planes, NZR >= 2H + 2K) — half the barriers of a wait/refill pair;
 //   * the per-point streams (delta, E) are prefetched into registers one plane ahead.
-// Trace (3 fields, RK2 midpoint feet): k_sl_trace, ring of 2H+2 slots with one plane
-// prefetched into registers (H = 2: the midpoint displacement dt/2 v has |floor| <= 1).
+//   * x window: warps whose x floors take two values read 5 columns at lane-uniform offsets
+//     (conflict-free) instead of 4 at per-lane offsets (a 33-column span: 2 wavefronts/tap).
+// Trace (3 fields, RK2 midpoint feet, H = 2: the midpoint displacement dt/2 v has |floor| <= 1):
+// k_sl_trace2 (default) computes column pairs (z, z+1) from a fixed 5 x 5 x 6 window shared by
+// both feet and both points; k_sl_trace (TOPT_TRACE2=0) one point per thread per plane.
 #include <cmath>
 
 #include "internal.cuh"
