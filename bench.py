@@ -244,9 +244,21 @@ def run_topt(args):
     torch.cuda.empty_cache()  # the generator's device temporaries (512^3: ~100 GB cached)
     cfgp = dict(n=tuple(d["n"]), nt=d["nt"], model=d["model"], reg_order=d["reg_order"], alpha=d["alpha"])
     slab = world > 1 and args.parallel == "slab"
+    slab_error = None
     if slab:  # one z-slab per GPU over NCCL
         uid = share_unique_id(rank, world, topt.get_unique_id)
-        t = topt.Topt(topt.Config(window=d["window"], **cfgp), device=dev, rank=rank, world=world, unique_id=uid)
+        t, err = None, 0.0
+        try:
+            t = topt.Topt(topt.Config(window=d["window"], **cfgp), device=dev, rank=rank, world=world,
+                          unique_id=uid)
+        except Exception as e:  # e.g. the NCCL communicator cannot be created on this node
+            slab_error, err = f"{type(e).__name__}: {e}"[:200], 1.0
+        if max_over_ranks(err, world, dev) > 0:  # every rank falls back together
+            slab, t = False, None
+            slab_error = slab_error or "z-slab context failed on another rank"
+            if rank == 0:
+                sys.stderr.write(f"bench: z-slab path unavailable ({slab_error}); running replicas\n")
+    if slab:
         m0n, m1n = slab_of(d["m0"], rank, world), slab_of(d["m1"], rank, world)
         vn = slab_of(d["vstar"], rank, world, vector=True)
     else:
@@ -418,6 +430,7 @@ def run_topt(args):
             "config": {"workload": wl, "grid": list(d["n"]), "nt": d["nt"], "model": d["model"],
                        "reg_order": d["reg_order"], "alpha": d["alpha"],
                        "parallelism": (f"zslab{world}" if slab else f"replicas{world}") if world > 1 else "single",
+                       **({"zslab_error": slab_error} if slab_error else {}),
                        "l2": "inputs larger than L2 (~15 GB of HBM traffic per evaluation vs 126 MB L2)"},
             "clocks": clk.summary(),
             "e2e": e2e,
