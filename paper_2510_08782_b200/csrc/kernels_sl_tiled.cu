@@ -67,6 +67,15 @@ __device__ __forceinline__ void lag4(float t, float w[4]) {
   w[3] = fmaf(t, c6, c6);
 }
 
+// base + idx (idx < 2^32 floats) as ONE mad.wide.u32 (the generic form costs a 32-bit add and
+// a 64-bit shift-add pair per address)
+template <typename T>
+__device__ __forceinline__ T* at_u32(T* base, unsigned idx) {
+  T* r;
+  asm("mad.wide.u32 %0, %1, 4, %2;" : "=l"(r) : "r"(idx), "l"(base));
+  return r;
+}
+
 // Global-memory (L1) gather, periodic; fallback for feet outside the halo.
 __device__ __forceinline__ float gather_global(const Geom& g, const float* __restrict__ f, int x, int y, int z,
                                                float dx, float dy, float dz) {
@@ -241,10 +250,10 @@ __global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, T
   float n0, n1, n2, nE = 1.0f;
   auto fetch = [&](int zi) {
     const unsigned o = (unsigned)zi * P32;
-    n0 = __ldg(pd + o);
-    n1 = __ldg(pd + (F32 + o));
-    n2 = __ldg(pd + (2u * F32 + o));
-    if (HAS_E) nE = __ldg(pE + o);
+    n0 = __ldg(at_u32(pd, o));
+    n1 = __ldg(at_u32(pd, F32 + o));
+    n2 = __ldg(at_u32(pd, 2u * F32 + o));
+    if (HAS_E) nE = __ldg(at_u32(pE, o));
   };
   fetch(0);
   double acc = 0.0;
@@ -322,11 +331,11 @@ __global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, T
       }
       if (MODE == M_EFACTOR) {
         const float bv = sm[(z & (NZR - 1)) * PS + (ty + H) * PW + tx + XH];  // divv(l)
-        pout[o] = 1.0f + a.sh * (r + bv) + a.h2 * r * bv;
+        *at_u32(pout, o) = 1.0f + a.sh * (r + bv) + a.h2 * r * bv;
       } else {
         float val = r;
         if (HAS_E) val *= cE;
-        pout[o] = val;
+        *at_u32(pout, o) = val;
         if (MODE == M_LAST) {
           const size_t gi = gi0 + o;
           const float res = __ldg(a.m1 + gi) - val;
