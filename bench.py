@@ -251,6 +251,8 @@ def run_topt(args):
         try:
             t = topt.Topt(topt.Config(window=d["window"], **cfgp), device=dev, rank=rank, world=world,
                           unique_id=uid)
+            if args.transport == "p2p":
+                t.enable_p2p()
         except Exception as e:  # e.g. the NCCL communicator cannot be created on this node
             slab_error, err = f"{type(e).__name__}: {e}"[:200], 1.0
         if max_over_ranks(err, world, dev) > 0:  # every rank falls back together
@@ -387,6 +389,8 @@ def run_topt(args):
         if slab:  # a fresh NCCL unique id per communicator
             uid2 = share_unique_id(rank, world, topt.get_unique_id)
             ts = topt.Topt(topt.Config(**kw), device=dev, rank=rank, world=world, unique_id=uid2)
+            if args.transport == "p2p":
+                ts.enable_p2p()
         else:
             ts = topt.Topt(topt.Config(**kw), device=dev)
         ts.solve(m0, m1)  # warm-up
@@ -430,6 +434,7 @@ def run_topt(args):
             "config": {"workload": wl, "grid": list(d["n"]), "nt": d["nt"], "model": d["model"],
                        "reg_order": d["reg_order"], "alpha": d["alpha"],
                        "parallelism": (f"zslab{world}" if slab else f"replicas{world}") if world > 1 else "single",
+                       **({"transport": args.transport} if slab else {}),
                        **({"zslab_error": slab_error} if slab_error else {}),
                        "l2": "inputs larger than L2 (~15 GB of HBM traffic per evaluation vs 126 MB L2)"},
             "clocks": clk.summary(),
@@ -461,6 +466,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--solver-iters", type=int, default=4, help="GA-NGMRES iterations timed (0: skip)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
+                    help="z-slabs: z<->y transposes by NCCL send/recv or by P2P pulls over CUDA IPC")
     ap.add_argument("--parallel", default="slab", choices=["slab", "replica"],
                     help="N > 1: z-slabs over NCCL (one problem) or independent replicas")
     args = ap.parse_args()

@@ -153,6 +153,21 @@ topt_status topt_bind_workspace(topt_ctx* ctx, void* dptr, size_t bytes);
 /* Local z-slab of this rank: planes [z0, z0 + nz). */
 topt_status topt_local_slab(const topt_ctx* ctx, int32_t* z0, int32_t* nz);
 
+/* z-slabs (world > 1): transport of the z<->y all-to-all transposes.
+ * 0 (default) = pack + grouped ncclSend/ncclRecv + unpack; 1 = P2P pull: each rank reads its
+ * chunks straight from the peers' slabs over NVLink (no pack / unpack passes), ordered by
+ * one-byte all-reduce barriers.  With one process per GPU, transport 1 needs
+ * topt_set_peer_workspaces first; with emulated slabs (one process) it runs the same pull
+ * kernel on the local slabs.  Transposes whose source is not in the workspace keep NCCL.
+ * TOPT_ERR_INVALID_ARG for another value. */
+topt_status topt_set_transport(topt_ctx* ctx, int32_t transport);
+
+/* Peer workspaces for transport 1: bases[r] = rank r's bound workspace pointer (as passed to
+ * its topt_bind_workspace) mapped into THIS process (CUDA IPC; bases[rank] = this rank's own),
+ * count == world.  The pointers are borrowed: the caller keeps the mappings alive while the
+ * context uses them.  count == 0 clears them.  TOPT_ERR_INVALID_ARG on a count mismatch. */
+topt_status topt_set_peer_workspaces(topt_ctx* ctx, void* const* bases, int32_t count);
+
 /* ---- solver --------------------------------------------------------------------- */
 
 /* GA-NGMRES(w; sigma, tau) (Alg. 3) or GA-AA from v^0 = v_inout (the

@@ -111,7 +111,26 @@ class Topt:
         off = (-base) % 256
         check(LIB.topt_bind_workspace(self.ctx, ctypes.c_void_p(base + off), nbytes.value),
               "topt_bind_workspace")
+        self._ws_off = off
         self.scalars = torch.zeros(_lib.NSCALARS, dtype=torch.float64, device=self.device)
+
+    # -- z-slab transport
+    def set_transport(self, transport: str = "nccl"):
+        """z<->y transposes: "nccl" (pack + send/recv + unpack) or "p2p" (pull from the peers'
+        slabs; emulated slabs: the same pull kernel on the local slabs)."""
+        check(LIB.topt_set_transport(self.ctx, {"nccl": 0, "p2p": 1}[transport]), "topt_set_transport")
+
+    def enable_p2p(self, group=None):
+        """One process per GPU: map every rank's workspace into this process (CUDA IPC through
+        torch's CUDA tensor sharing, handles exchanged with torch.distributed) and switch the
+        transposes to P2P pulls.  Collective: every rank calls it."""
+        maps, offs = map_peer_tensors(self.workspace, self.rank, self.world, self._ws_off, group)
+        self._peer_maps = maps  # keeps the mappings alive as long as this context
+        bases = (ctypes.c_void_p * self.world)()
+        for r in range(self.world):
+            bases[r] = maps[r].data_ptr() + offs[r]
+        check(LIB.topt_set_peer_workspaces(self.ctx, bases, self.world), "topt_set_peer_workspaces")
+        self.set_transport("p2p")
 
     def __del__(self):
         try:
@@ -259,6 +278,21 @@ class Topt:
         out = rep.as_dict()
         out["exit_name"] = EXIT.get(rep.exit, rep.exit)
         return v, out
+
+
+def map_peer_tensors(t, rank: int, world: int, tag=None, group=None):
+    """Collective over the process group: every rank's CUDA tensor `t` mapped into this process
+    (CUDA IPC via torch's CUDA tensor sharing; rank `rank`'s own entry is `t` itself).  Returns
+    (tensors, tags) indexed by rank; the mapped tensors must stay alive while they are used."""
+    import torch.distributed as dist
+    from torch.multiprocessing.reductions import reduce_tensor
+    objs = [None] * world
+    dist.all_gather_object(objs, (reduce_tensor(t), tag), group=group)
+    maps, tags = [], []
+    for r, ((fn, args), tg) in enumerate(objs):
+        maps.append(t if r == rank else fn(*args))
+        tags.append(tg)
+    return maps, tags
 
 
 def get_unique_id() -> bytes:

@@ -308,6 +308,25 @@ topt_status topt_bind_workspace(topt_ctx* c, void* dptr, size_t bytes) {
   return TOPT_OK;
 }
 
+topt_status topt_set_transport(topt_ctx* ctx, int32_t transport) {
+  if (!ctx) return fail(TOPT_ERR_INVALID_ARG, "NULL context");
+  if (transport != 0 && transport != 1) return fail(TOPT_ERR_INVALID_ARG, "transport must be 0 or 1");
+  ctx->comm.transport = transport;
+  return TOPT_OK;
+}
+
+topt_status topt_set_peer_workspaces(topt_ctx* ctx, void* const* bases, int32_t count) {
+  if (!ctx) return fail(TOPT_ERR_INVALID_ARG, "NULL context");
+  if (count == 0) {
+    ctx->comm.peer_ws.clear();
+    return TOPT_OK;
+  }
+  if (count != ctx->comm.P || !bases) return fail(TOPT_ERR_INVALID_ARG, "count must equal the world size");
+  ctx->comm.peer_ws.assign(count, nullptr);
+  for (int r = 0; r < count; ++r) ctx->comm.peer_ws[r] = static_cast<char*>(bases[r]);
+  return TOPT_OK;
+}
+
 topt_status topt_local_slab(const topt_ctx* ctx, int32_t* z0, int32_t* nz) {
   if (!ctx || !z0 || !nz) return fail(TOPT_ERR_INVALID_ARG, "NULL argument");
   const bool emu = ctx->comm.P > 1 && ctx->comm.emulated();

@@ -52,9 +52,15 @@ struct Slab {
 };
 
 // Communicator over the P slabs.  nloc == P: all slabs local (device copies); nloc == 1: NCCL.
+// transport (z<->y transposes): 0 = pack + grouped ncclSend/ncclRecv + unpack; 1 = P2P pull —
+// each rank reads its chunks straight from the peers' slabs (peer_ws: every rank's workspace
+// base mapped into this process, CUDA IPC), stream-ordered by one-byte all-reduce barriers.
+// Emulated slabs run the same pull kernel on the local slab pointers.
 struct Comm {
   int P = 1;
   int nloc = 1;
+  int transport = 0;
+  std::vector<char*> peer_ws;
 #ifdef TOPT_WITH_NCCL
   ncclComm_t nccl = nullptr;
 #endif

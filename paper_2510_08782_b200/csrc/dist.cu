@@ -7,8 +7,12 @@
 //     and the all-to-all, ncclAllReduce for scalars;
 //   * emulation (all P slabs in one process on one GPU): the same data movement as device
 //     copies — used by the tests to check that P slabs reproduce the single-slab result.
+//   * P2P pull (transport 1, z<->y transposes): each rank reads its chunks straight from the
+//     peers' slabs through CUDA-IPC-mapped workspaces (no pack / unpack passes, no NCCL
+//     send/recv), ordered by one-byte all-reduce barriers before and after.
 // Layouts: z-slab [nz/P][ny][nx] (halo'd inputs: [zh + nz/P + zh] planes); y-slab
 // [nz][ny/P][nx].  The chunk exchanged between slabs r and q is nz/P x ny/P x nx elements.
+#include <algorithm>
 #include <cstdio>
 
 #include "ctx.cuh"
@@ -39,7 +43,83 @@ __global__ void k_allreduce_emul(PtrList L, int nslab, int count, int is_max) {
   for (int s = 0; s < nslab; ++s) L.p[s][i] = acc;
 }
 
+// P2P pull of one transpose (z->y if Z2Y, else y->z) for local rank r: 16-byte vectors of
+// the P chunks, chunk q read from src[q] (rank q's buffer, local or peer-mapped).  z->y: my
+// y-slab chunk q (planes of rank q, my rows) <- rank q's z-slab rows [r nyl, (r+1) nyl);
+// y->z: my z-slab rows [q nyl, (q+1) nyl) <- rank q's y-slab chunk r.
+struct SrcList {
+  const char* p[64];
+};
+template <bool Z2Y>
+__global__ void k_pull(char* __restrict__ dst, SrcList src, int P, int r, int nzl, int nyl, size_t rowb,
+                       size_t pitch, size_t w, size_t chunk) {
+  const size_t nv = rowb / 16, per = (size_t)nzl * nyl * nv, total = per * P;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int q = (int)(i / per);
+    size_t j = i % per;
+    const size_t v = j % nv;
+    j /= nv;
+    const int y = (int)(j % nyl), pl = (int)(j / nyl);
+    size_t so, dof;
+    if (Z2Y) {
+      dof = q * chunk + pl * w + y * rowb + 16 * v;
+      so = pl * pitch + ((size_t)r * nyl + y) * rowb + 16 * v;
+    } else {
+      so = r * chunk + pl * w + y * rowb + 16 * v;
+      dof = pl * pitch + ((size_t)q * nyl + y) * rowb + 16 * v;
+    }
+    // .cv: peer memory is read around the local caches (no stale lines from an earlier pull)
+    *reinterpret_cast<uint4*>(dst + dof) = __ldcv(reinterpret_cast<const uint4*>(src.p[q] + so));
+  }
+}
+
 }  // namespace
+
+// stream-ordered barrier over the ranks (every rank's earlier work on `st` is complete when
+// it returns on the device): a one-byte all-reduce
+static bool comm_barrier(topt_ctx* c, cudaStream_t st) {
+#ifdef TOPT_WITH_NCCL
+  char* b = c->slabs[0].sendbuf;
+  return nccl_ok(ncclAllReduce(b, b, 1, ncclChar, ncclSum, c->comm.nccl, st), "ncclAllReduce(barrier)");
+#else
+  (void)c;
+  (void)st;
+  return false;
+#endif
+}
+
+// a P2P pull needs the source inside the workspace (same offset on every rank); others (a
+// caller's v, for instance) take the NCCL path
+static bool pull_ok(const topt_ctx* c, const std::vector<const char*>& src) {
+  if (c->comm.transport != 1) return false;
+  if (c->comm.emulated()) return true;
+  return (int)c->comm.peer_ws.size() == c->comm.P && src[0] >= c->ws && src[0] < c->ws + c->ws_bytes;
+}
+
+// z->y (Z2Y) or y->z transpose by P2P pull
+static bool comm_pull(topt_ctx* c, bool z2y, const std::vector<const char*>& src, const std::vector<char*>& dst,
+                      size_t eb, cudaStream_t st) {
+  const Comm& cm = c->comm;
+  const Slab& s0 = c->slabs[0];
+  const int P = cm.P, nzl = s0.g.nz, nyl = s0.g.ny / P, nx = s0.g.nx;
+  const size_t rowb = (size_t)nx * eb, w = nyl * rowb, pitch = (size_t)s0.g.ny * rowb, chunk = w * nzl;
+  if (P > 64 || rowb % 16) return false;
+  const bool emu = cm.emulated();
+  if (!emu && !comm_barrier(c, st)) return false;  // every rank's source is complete
+  const size_t vec = (size_t)P * nzl * nyl * (rowb / 16);
+  const int blocks = (int)std::min<size_t>((vec + 255) / 256, 148 * 16);
+  for (int r = 0; r < cm.nloc; ++r) {
+    const int rank = emu ? r : c->slabs[0].index;
+    SrcList L{};
+    for (int q = 0; q < P; ++q)
+      L.p[q] = emu ? src[q] : (q == rank ? src[0] : cm.peer_ws[q] + (src[0] - c->ws));
+    if (z2y) k_pull<true><<<blocks, 256, 0, st>>>(dst[r], L, P, rank, nzl, nyl, rowb, pitch, w, chunk);
+    else k_pull<false><<<blocks, 256, 0, st>>>(dst[r], L, P, rank, nzl, nyl, rowb, pitch, w, chunk);
+    count_launch();
+  }
+  if (cudaGetLastError() != cudaSuccess) return false;
+  return emu || comm_barrier(c, st);  // no rank overwrites a source another is still reading
+}
 
 // Halo planes of nf fields (field f of slab s at base[s] + f * fstride floats, layout
 // [zh + nzl + zh] planes of `plane` floats): low halo <- previous slab's top zh local planes,
@@ -82,6 +162,7 @@ bool comm_halo(topt_ctx* c, const std::vector<float*>& base, int nf, size_t fstr
 bool comm_z2y(topt_ctx* c, const std::vector<const char*>& src, const std::vector<char*>& dst, size_t eb,
               cudaStream_t st) {
   const Comm& cm = c->comm;
+  if (pull_ok(c, src)) return comm_pull(c, true, src, dst, eb, st);
   const Slab& s0 = c->slabs[0];
   const int P = cm.P, nzl = s0.g.nz, nyl = s0.g.ny / P, nx = s0.g.nx;
   const size_t w = (size_t)nyl * nx * eb, spitch = (size_t)s0.g.ny * nx * eb, chunk = w * nzl;
@@ -111,6 +192,7 @@ bool comm_z2y(topt_ctx* c, const std::vector<const char*>& src, const std::vecto
 bool comm_y2z(topt_ctx* c, const std::vector<const char*>& src, const std::vector<char*>& dst, size_t eb,
               cudaStream_t st) {
   const Comm& cm = c->comm;
+  if (pull_ok(c, src)) return comm_pull(c, false, src, dst, eb, st);
   const Slab& s0 = c->slabs[0];
   const int P = cm.P, nzl = s0.g.nz, nyl = s0.g.ny / P, nx = s0.g.nx;
   const size_t w = (size_t)nyl * nx * eb, dpitch = (size_t)s0.g.ny * nx * eb, chunk = w * nzl;

@@ -12,15 +12,19 @@ from oracle import spectral
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
 @pytest.mark.parametrize("model", [0, 1, 2])
 @pytest.mark.parametrize("P", [2, 4, 8])
-def test_eval_gradient_slab_invariance(model, P):
+def test_eval_gradient_slab_invariance(model, P, transport):
+    """transport "nccl": the emulated pack / send-recv / unpack copies; "p2p": the pull kernel
+    reading every chunk straight from the owning slab (the kernel of the CUDA-IPC transport)."""
     d = case(2, (64, 32, 32), model=model)
     if model == 2:
         d["v"] = spectral.leray(d["grid"], d["v"]).astype(np.float32).astype(np.float64)
     t1 = topt_for(d)
     g1, s1, sc1 = t1.eval_gradient(dev(d["m0"]), dev(d["m1"]), dev(d["v"]))
     tp = topt_for(d, world=P)
+    tp.set_transport(transport)
     gp, sp, scp = tp.eval_gradient(dev(d["m0"]), dev(d["m1"]), dev(d["v"]))
     g1, s1, gp, sp = host(g1), host(s1), host(gp), host(sp)
     assert rel_l2(gp, g1) < 1e-6
@@ -53,6 +57,35 @@ def test_solve_slab_invariance(P):
     assert rp["iters"] == r1["iters"] == 12
     assert abs(rp["obj"] - r1["obj"]) <= 1e-5 * abs(r1["obj"])
     assert rel_l2(host(vp), host(v1)) < 1e-4
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_p2p_pull_equals_copy_transport_bitwise(P):
+    """Both transports move the same bytes: the evaluation and a short solve agree bitwise."""
+    d = case(2, (64, 32, 32), model=1)
+    out = {}
+    for tr in ("nccl", "p2p"):
+        t = topt_for(d, world=P, max_iter=3, eps_rel=0.0)
+        t.set_transport(tr)
+        g, s, sc = t.eval_gradient(dev(d["m0"]), dev(d["m1"]), dev(d["v"]))
+        v, rep = t.solve(dev(d["m0"]), dev(d["m1"]))
+        out[tr] = (host(g), host(s), host(v), rep["obj"])
+    for a, b in zip(out["nccl"][:3], out["p2p"][:3]):
+        assert np.array_equal(a, b)
+    assert out["nccl"][3] == out["p2p"][3]
+
+
+def test_transport_and_peer_arguments_checked():
+    import ctypes
+
+    import paper_2510_08782_b200 as topt
+    LIB = topt._lib.LIB
+    d = case(2, (32, 32, 32))
+    t = topt_for(d, world=2)
+    assert LIB.topt_set_transport(t.ctx, 5) != 0
+    bases = (ctypes.c_void_p * 3)()
+    assert LIB.topt_set_peer_workspaces(t.ctx, bases, 3) != 0   # count != world
+    assert LIB.topt_set_peer_workspaces(t.ctx, bases, 0) == 0   # clear
 
 
 def test_halo_overflow_is_reported():
