@@ -29,6 +29,9 @@ bool comm_z2y(topt_ctx* c, const std::vector<const char*>& src, const std::vecto
 bool comm_y2z(topt_ctx* c, const std::vector<const char*>& src, const std::vector<char*>& dst, size_t eb,
               cudaStream_t st);
 bool comm_allreduce(topt_ctx* c, const std::vector<double*>& ptr, int count, bool is_max, cudaStream_t st);
+bool comm_p2p_ready(const topt_ctx* c);
+char* comm_peer(const topt_ctx* c, const void* p, int q);
+bool comm_fence(topt_ctx* c, cudaStream_t st);
 }  // namespace topt
 
 namespace {
@@ -653,7 +656,25 @@ void backward_half(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
       launch_deriv_accum(sl.g, a, da, st);
     }
   }
-  if (P > 1) {  // z axis in the y-slab layout: transpose all S+1 slices of psi and lam
+  if (P > 1 && comm_p2p_ready(c)) {
+    // z axis, P2P transport: one kernel per rank reads the z-lines of its y rows from every
+    // rank's slices and writes b_z into every rank's slab (transposes fused away)
+    comm_fence(c, st);  // every rank's trajectories are complete
+    const bool emu = c->comm.emulated();
+    for (auto& sl : c->slabs) {
+      const float *ps[8], *ls[8];
+      float* os[8];
+      for (int q = 0; q < P; ++q) {
+        Slab& sq = emu ? c->slabs[q] : c->slabs[0];  // one process per GPU: peers by translation
+        ps[q] = (const float*)comm_peer(c, local(sq, cont ? sq.lam_traj : sq.m_traj), q);
+        ls[q] = (const float*)comm_peer(c, local(sq, cont ? sq.m_traj : sq.lam_traj), q);
+        os[q] = (float*)comm_peer(c, sq.b + 2 * F, q);
+      }
+      Prof pr(c, K_BODY, (2.0 * (S + 1) + 1.0) * F4, 1, st);
+      launch_deriv_zpull(sl.gy, ps, ls, os, P, sl.Fh, sl.Fh, sl.g.nz, sl.plane, w.data(), S + 1, st);
+    }
+    comm_fence(c, st);  // every rank's b_z is complete before it is read
+  } else if (P > 1) {  // z axis in the y-slab layout: transpose all S+1 slices of psi and lam
     for (int j = 0; j <= S; ++j)
       for (int which = 0; which < 2; ++which) {  // 0: psi, 1: lam
         std::vector<float*> src, dst;

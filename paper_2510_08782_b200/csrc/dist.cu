@@ -121,6 +121,19 @@ static bool comm_pull(topt_ctx* c, bool z2y, const std::vector<const char*>& src
   return emu || comm_barrier(c, st);  // no rank overwrites a source another is still reading
 }
 
+// public helpers of the P2P transport for fused kernels (api.cu): is it usable, the rank-q
+// image of a local workspace pointer, and the stream-ordered barrier (no-op when emulated)
+bool comm_p2p_ready(const topt_ctx* c) {
+  const Comm& cm = c->comm;
+  return cm.transport == 1 && cm.P <= 8 && (cm.emulated() || (int)cm.peer_ws.size() == cm.P);
+}
+char* comm_peer(const topt_ctx* c, const void* p, int q) {
+  const Comm& cm = c->comm;
+  if (cm.emulated() || q == c->slabs[0].index) return (char*)p;
+  return cm.peer_ws[q] + ((const char*)p - c->ws);
+}
+bool comm_fence(topt_ctx* c, cudaStream_t st) { return c->comm.emulated() || comm_barrier(c, st); }
+
 // Halo planes of nf fields (field f of slab s at base[s] + f * fstride floats, layout
 // [zh + nzl + zh] planes of `plane` floats): low halo <- previous slab's top zh local planes,
 // high halo <- next slab's bottom zh local planes (ring, periodic in z).

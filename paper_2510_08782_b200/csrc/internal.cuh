@@ -89,6 +89,12 @@ struct DerivArgs {
   float* out;
 };
 void launch_deriv_accum(const Geom& g, int axis, const DerivArgs& a, cudaStream_t st);
+// z-slabs, P2P transport: body-force z pass on the y-slab rows of gy reading the slices of every
+// rank's z-slab directly (psi[q], lam[q]: rank q's slice 0, slices `stride` apart, nzl planes of
+// plane_src floats) and writing b_z into every rank's z-slab (out[q]); P <= 8
+void launch_deriv_zpull(const Geom& gy, const float* const* psi, const float* const* lam, float* const* out, int P,
+                        size_t psi_stride, size_t lam_stride, int nzl, size_t plane_src, const double* wts, int J,
+                        cudaStream_t st);
 
 // u = alpha L v (alpha L P_L v if leray); fp64 chain, Zv = 3 double2 fields of F
 void launch_vchain(const Geom& g, const float* v, double2* Zv, float* u, double alpha, int p, bool leray,

@@ -246,6 +246,100 @@ __global__ void __launch_bounds__(kThreads, (EMAX == 8 || N == 256 ? TOPT_RDS16_
   }
 }
 
+// z-slabs, P2P transport: the z pass of the body force fused with both transposes.  The block
+// works on the y-slab rows of its rank (geometry gy: nz = global planes, ny = this rank's rows,
+// ky0 = their global offset) but reads every z-line element straight from the z-slab of the
+// rank owning that plane (pointer tables: rank q's slice-0 psi / lam, local or peer-mapped), and
+// writes b_z back into the owners' z-slabs — no y-slab copies of the 2(S+1) slices, no return
+// transpose.  Same arithmetic as k_rds (axis 2).
+struct ZTab {
+  const float* psi[8];
+  const float* lam[8];
+  float* out[8];
+};
+template <int N, int EMAX>
+__global__ void __launch_bounds__(kThreads, (EMAX == 8 || N == 256 ? TOPT_RDS16_MINB : 1)) k_rds_zpull(
+    Geom g, int TXC, ZTab tb, size_t psi_stride, size_t lam_stride, int lnzl, unsigned plane_src, DerivWeights w,
+    int J, int nitems) {
+  constexpr int E = Ev<N, EMAX>::v, T = N / E;
+  using R = RfCfg<N, E>;
+  extern __shared__ __align__(16) float2 smem[];
+  __shared__ const float* sps[8];
+  __shared__ const float* sls[8];
+  __shared__ float* sos[8];
+  if (threadIdx.x < 8) {
+    sps[threadIdx.x] = tb.psi[threadIdx.x];
+    sls[threadIdx.x] = tb.lam[threadIdx.x];
+    sos[threadIdx.x] = tb.out[threadIdx.x];
+  }
+  __syncthreads();
+  const int c = threadIdx.x % TXC, t = threadIdx.x / TXC;
+  float2* lbuf = smem + c * R::STRIDE;
+  float2 tw[R::NTW];
+  rf_twiddles<N, E>(tw, t);
+  const int tilesx = g.nx / (2 * TXC);
+  const float invN = 1.0f / (float)N;
+  const int zmask = (1 << lnzl) - 1;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int x0 = (item % tilesx) * 2 * TXC, outer = item / tilesx;
+    const unsigned yx = ((unsigned)(g.ky0 + outer) << g.lx) + x0 + 2 * c;  // (y, x) in a source plane
+    float2 acc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = make_float2(0.f, 0.f);
+    for (int j = 0; j < J; ++j) {
+      float2 z[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int zr = t + T * e;
+        z[e] = __ldcv(reinterpret_cast<const float2*>(sps[zr >> lnzl] + j * psi_stride + (zr & zmask) * plane_src + yx));
+      }
+      rf_fft<N, E, false, false>(z, lbuf, t, tw);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const float k = kprime(t + T * e, N) * invN;
+        z[e] = make_float2(-k * z[e].y, k * z[e].x);
+      }
+      rf_fft<N, E, true, false>(z, lbuf, t, tw);
+      const float wj = w.w[j];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int zr = t + T * e;
+        const float2 l = __ldcv(reinterpret_cast<const float2*>(sls[zr >> lnzl] + j * lam_stride + (zr & zmask) * plane_src + yx));
+        acc[e].x = fmaf(wj * l.x, z[e].x, acc[e].x);
+        acc[e].y = fmaf(wj * l.y, z[e].y, acc[e].y);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int zr = t + T * e;
+      *reinterpret_cast<float2*>(sos[zr >> lnzl] + (zr & zmask) * plane_src + yx) = acc[e];
+    }
+  }
+}
+
+static int ilog2i(int n) {
+  int l = 0;
+  while ((1 << l) < n) ++l;
+  return l;
+}
+
+template <int N>
+static void zpull_launch(const Geom& gy, const ZTab& tb, size_t psi_stride, size_t lam_stride, int nzl,
+                         unsigned plane_src, const DerivWeights& w, int J, cudaStream_t st) {
+  constexpr int EMAX = 16;
+  constexpr int E = Ev<N, EMAX>::v, T = N / E;
+  using R = RfCfg<N, E>;
+  int TXC = kThreads / T;
+  if (2 * TXC > gy.nx) TXC = gy.nx / 2;
+  const int threads = TXC * T;
+  const size_t sm = (size_t)TXC * R::STRIDE * sizeof(float2);
+  const long long items = (long long)(gy.nx / (2 * TXC)) * gy.ny;
+  const int blocks = persistent_blocks(k_rds_zpull<N, EMAX>, threads, sm, items);
+  k_rds_zpull<N, EMAX><<<blocks, threads, sm, st>>>(gy, TXC, tb, psi_stride, lam_stride, ilog2i(nzl), plane_src, w,
+                                                    J, (int)items);
+  count_launch();
+}
+
 // Body force along a strided axis (J time slices): as k_rds, but the psi tile of slice j+1
 // and the lam tile of slice j are copied global -> shared with cp.async while slice j is
 // transformed, so the HBM latency of both streams hides behind the line FFTs (no extra
@@ -408,6 +502,20 @@ static void deriv_dispatch(const Geom& g, int axis, const DerivArgs& a, const De
     case 1024: FN<1024>(__VA_ARGS__); break;           \
     default: fprintf(stderr, "topt: unsupported N %d\n", NV); \
   }
+
+void launch_deriv_zpull(const Geom& gy, const float* const* psi, const float* const* lam, float* const* out, int P,
+                        size_t psi_stride, size_t lam_stride, int nzl, size_t plane_src, const double* wts, int J,
+                        cudaStream_t st) {
+  ZTab tb{};
+  for (int q = 0; q < P && q < 8; ++q) {
+    tb.psi[q] = psi[q];
+    tb.lam[q] = lam[q];
+    tb.out[q] = out[q];
+  }
+  DerivWeights w;
+  for (int j = 0; j < J && j < kMaxWeights; ++j) w.w[j] = (float)wts[j];
+  TOPT_DISPATCH_N(gy.nz, zpull_launch, gy, tb, psi_stride, lam_stride, nzl, (unsigned)plane_src, w, J, st);
+}
 
 void launch_deriv_accum(const Geom& g, int axis, const DerivArgs& a, cudaStream_t st) {
   DerivWeights w;
