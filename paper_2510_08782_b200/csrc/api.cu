@@ -465,9 +465,10 @@ void compute_div(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
   }
   if (P > 1) {
     std::vector<float*> src, dst, ysrc, back;
-    for (size_t si = 0; si < c->slabs.size(); ++si) {
-      src.push_back(const_cast<float*>(io[si].v) + 2 * c->slabs[si].F);
-      dst.push_back(c->slabs[si].ytmp);
+    for (size_t si = 0; si < c->slabs.size(); ++si) {  // v_z from the workspace copy (P2P-pullable)
+      Slab& sl = c->slabs[si];
+      src.push_back(local(sl, sl.vh + 2 * sl.Fh));
+      dst.push_back(sl.ytmp);
     }
     tz2y(c, src, dst, st);
     for (auto& sl : c->slabs) {
