@@ -46,13 +46,15 @@ def test_objective_slab_invariance():
         assert abs(o1[k] - o4[k]) <= 1e-6 * abs(o1[k]), k
 
 
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
 @pytest.mark.parametrize("P", [2, 8])
-def test_solve_slab_invariance(P):
-    """20 GA-NGMRES iterations on P emulated slabs vs one slab (replayed step sequence)."""
+def test_solve_slab_invariance(P, transport):
+    """12 GA-NGMRES iterations on P emulated slabs vs one slab."""
     d = case(2, (64, 32, 32))
     t1 = topt_for(d, max_iter=12, eps_rel=0.0)
     v1, r1 = t1.solve(dev(d["m0"]), dev(d["m1"]))
     tp = topt_for(d, world=P, max_iter=12, eps_rel=0.0)
+    tp.set_transport(transport)
     vp, rp = tp.solve(dev(d["m0"]), dev(d["m1"]))
     assert rp["iters"] == r1["iters"] == 12
     assert abs(rp["obj"] - r1["obj"]) <= 1e-5 * abs(r1["obj"])
