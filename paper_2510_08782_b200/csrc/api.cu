@@ -483,6 +483,22 @@ void compute_div(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
   }
 }
 
+// P2P transport, 3D non-Leray: the tables of nf fields (field f of slab q at base(slab) + f F)
+// for the in-place last-axis passes on the distributed slabs; false when not applicable
+template <typename T, typename Base>
+static bool remote_fields(topt_ctx* c, Base base, int nf, std::vector<const void*>& tab) {
+  const int P = P_of(c);
+  if (P == 1 || c->d != 3 || c->p.model == TOPT_INCOMPRESSIBLE || !comm_p2p_ready(c)) return false;
+  const bool emu = c->comm.emulated();
+  tab.assign((size_t)nf * P, nullptr);
+  for (int f = 0; f < nf; ++f)
+    for (int q = 0; q < P; ++q) {
+      Slab& sq = emu ? c->slabs[q] : c->slabs[0];
+      tab[(size_t)f * P + q] = comm_peer(c, (const T*)base(sq) + (size_t)f * c->F, q);
+    }
+  return true;
+}
+
 // u = alpha L v by the fp64 v-chain (P_L first for incompressible, R9) into utmp; io[].u := utmp
 void run_vchain(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
   const int P = P_of(c);
@@ -502,23 +518,31 @@ void run_vchain(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
       double2* Z[3] = {sl.Zv, sl.Zv + F, sl.Zv + 2 * F};
       vchain_xy(sl.g, io[si].v, Z, leray, st);
     }
-    if (P > 1)
-      for (int f = 0; f < vin; ++f) {
-        std::vector<double2*> a, b;
-        for (auto& sl : c->slabs) { a.push_back(sl.Zv + f * F); b.push_back(sl.Zvy + f * F); }
-        tz2y(c, a, b, st);
+    std::vector<const void*> rtab;
+    if (remote_fields<double2>(c, [](Slab& s) { return s.Zv; }, vin, rtab)) {
+      comm_fence(c, st);  // every rank's x, y passes are complete
+      for (auto& sl : c->slabs)
+        vchain_last_remote(sl.gy, rtab.data(), P, sl.g.nz, sl.plane, c->p.alpha, c->p.reg_order, n_all, st);
+      comm_fence(c, st);  // every rank's z lines are transformed
+    } else {
+      if (P > 1)
+        for (int f = 0; f < vin; ++f) {
+          std::vector<double2*> a, b;
+          for (auto& sl : c->slabs) { a.push_back(sl.Zv + f * F); b.push_back(sl.Zvy + f * F); }
+          tz2y(c, a, b, st);
+        }
+      for (auto& sl : c->slabs) {
+        double2* base = P > 1 ? sl.Zvy : sl.Zv;
+        double2* Z[3] = {base, base + F, base + 2 * F};
+        vchain_last(P > 1 ? sl.gy : sl.g, Z, c->p.alpha, c->p.reg_order, leray, n_all, st);
       }
-    for (auto& sl : c->slabs) {
-      double2* base = P > 1 ? sl.Zvy : sl.Zv;
-      double2* Z[3] = {base, base + F, base + 2 * F};
-      vchain_last(P > 1 ? sl.gy : sl.g, Z, c->p.alpha, c->p.reg_order, leray, n_all, st);
+      if (P > 1)
+        for (int f = 0; f < vout; ++f) {
+          std::vector<double2*> a, b;
+          for (auto& sl : c->slabs) { a.push_back(sl.Zvy + f * F); b.push_back(sl.Zv + f * F); }
+          ty2z(c, a, b, st);
+        }
     }
-    if (P > 1)
-      for (int f = 0; f < vout; ++f) {
-        std::vector<double2*> a, b;
-        for (auto& sl : c->slabs) { a.push_back(sl.Zvy + f * F); b.push_back(sl.Zv + f * F); }
-        ty2z(c, a, b, st);
-      }
     for (size_t si = 0; si < c->slabs.size(); ++si) {
       Slab& sl = c->slabs[si];
       double2* Z[3] = {sl.Zv, sl.Zv + F, sl.Zv + 2 * F};
@@ -752,23 +776,31 @@ void backward_half(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
       float2* Z[4] = {sl.Z, sl.Z + F, sl.Z + 2 * F, sl.Z + 3 * F};
       bchain_xy(sl.g, sl.b, Z, leray, st);
     }
-    if (P > 1)
-      for (int f = 0; f < bin; ++f) {
-        std::vector<float2*> a, b;
-        for (auto& sl : c->slabs) { a.push_back(sl.Z + f * F); b.push_back(sl.Zy + f * F); }
-        tz2y(c, a, b, st);
+    std::vector<const void*> rtab;
+    if (remote_fields<float2>(c, [](Slab& s) { return s.Z; }, bin, rtab)) {
+      comm_fence(c, st);
+      for (auto& sl : c->slabs)
+        bchain_last_remote(sl.gy, rtab.data(), P, sl.g.nz, sl.plane, c->p.alpha, c->p.reg_order, n_all, st);
+      comm_fence(c, st);
+    } else {
+      if (P > 1)
+        for (int f = 0; f < bin; ++f) {
+          std::vector<float2*> a, b;
+          for (auto& sl : c->slabs) { a.push_back(sl.Z + f * F); b.push_back(sl.Zy + f * F); }
+          tz2y(c, a, b, st);
+        }
+      for (auto& sl : c->slabs) {
+        float2* base = P > 1 ? sl.Zy : sl.Z;
+        float2* Z[4] = {base, base + F, base + 2 * F, base + 3 * F};
+        bchain_last(P > 1 ? sl.gy : sl.g, Z, c->p.alpha, c->p.reg_order, leray, n_all, st);
       }
-    for (auto& sl : c->slabs) {
-      float2* base = P > 1 ? sl.Zy : sl.Z;
-      float2* Z[4] = {base, base + F, base + 2 * F, base + 3 * F};
-      bchain_last(P > 1 ? sl.gy : sl.g, Z, c->p.alpha, c->p.reg_order, leray, n_all, st);
+      if (P > 1)
+        for (int f = 0; f < bout; ++f) {
+          std::vector<float2*> a, b;
+          for (auto& sl : c->slabs) { a.push_back(sl.Zy + f * F); b.push_back(sl.Z + f * F); }
+          ty2z(c, a, b, st);
+        }
     }
-    if (P > 1)
-      for (int f = 0; f < bout; ++f) {
-        std::vector<float2*> a, b;
-        for (auto& sl : c->slabs) { a.push_back(sl.Zy + f * F); b.push_back(sl.Z + f * F); }
-        ty2z(c, a, b, st);
-      }
     for (auto& sl : c->slabs) {
       float2* Z[4] = {sl.Z, sl.Z + F, sl.Z + 2 * F, sl.Z + 3 * F};
       bchain_yinv(sl.g, Z, leray, st);

@@ -110,6 +110,12 @@ void vchain_xy(const Geom& g, const float* v, double2* const* Z, bool leray, cud
 void vchain_last(const Geom& gz, double2* const* Z, double alpha, int p, bool leray, double n_total,
                  cudaStream_t st);
 void vchain_inv(const Geom& g, double2* const* Z, float* u, cudaStream_t st);
+// z-slabs, P2P transport (3D, non-Leray): the last-axis passes in place on the distributed
+// z-slabs; tab[f * P + q] = rank q's field f, nzl planes per rank of plane_src elements
+void vchain_last_remote(const Geom& gy, const void* const* tab, int P, int nzl, size_t plane_src, double alpha, int p,
+                        double n_total, cudaStream_t st);
+void bchain_last_remote(const Geom& gy, const void* const* tab, int P, int nzl, size_t plane_src, double alpha, int p,
+                        double n_total, cudaStream_t st);
 void bchain_xy(const Geom& g, const float* b, float2* const* Z, bool leray, cudaStream_t st);
 void bchain_last(const Geom& gz, float2* const* Z, double alpha, int p, bool leray, double n_total,
                  cudaStream_t st);

@@ -627,9 +627,23 @@ struct SpecOp {
 
 __device__ __forceinline__ double regL(double kk, int p) { return p == 1 ? kk : (p == 2 ? kk * kk : kk * kk * kk); }
 
-template <int N, int EMAX, int MODE, typename C>
+// z-slabs, P2P transport: the last-axis pass of a single-field mode (MODE <= 3) run in place on
+// the distributed z-slabs — element (z, y, x) of field f lives in rank z / nzl's slab at plane
+// z % nzl (tab[f][q]: rank q's field base, local or peer-mapped) — so neither transpose exists.
+struct RemoteZ {
+  int lnzl;            // log2 of the planes per rank
+  unsigned plane_src;  // elements per z-slab plane (nx * global ny)
+  const void* tab[4][8];
+};
+template <int N, int EMAX, int MODE, typename C, bool REM = false>
 __global__ void __launch_bounds__(kThreads, (MODE >= 4 ? 1 : 2)) k_rstrided(Geom g, int axis, int TXC, int NIN, int NOUT, ZList<C> Z,
-                                                       SpecOp op, int nitems) {
+                                                       SpecOp op, int nitems, RemoteZ rz = RemoteZ{}) {
+  static_assert(!REM || MODE <= 3, "remote addressing: single-field modes");
+  __shared__ C* rtab[REM ? 32 : 1];
+  if constexpr (REM) {
+    if (threadIdx.x < 32) rtab[threadIdx.x] = (C*)rz.tab[threadIdx.x >> 3][threadIdx.x & 7];
+    __syncthreads();
+  }
   constexpr int E = Ev<N, EMAX>::v, T = N / E;
   constexpr int NF = MODE >= 4 ? 3 : 1;  // fields held in registers
   using R = RfCfg<N, E>;
@@ -667,8 +681,16 @@ __global__ void __launch_bounds__(kThreads, (MODE >= 4 ? 1 : 2)) k_rstrided(Geom
     if constexpr (MODE <= 3) {
       C a[E];
       const C* src = Z.z[f0];
+      // remote: (y, x) offset inside a z-slab plane and the owner / plane of row zr
+      const unsigned yx = REM ? ((unsigned)(outer + g.ky0) << g.lx) + x0 + c : 0u;
+      auto rem = [&](int zr) -> C* {
+        return rtab[f0 * 8 + (zr >> rz.lnzl)] + (size_t)(zr & ((1 << rz.lnzl) - 1)) * rz.plane_src + yx;
+      };
 #pragma unroll
-      for (int e = 0; e < E; ++e) a[e] = src[base + (t + T * e) * Su];
+      for (int e = 0; e < E; ++e) {
+        if constexpr (REM) a[e] = __ldcv(rem(t + T * e));  // peer memory: around the local caches
+        else a[e] = src[base + (t + T * e) * Su];
+      }
       if constexpr (MODE != 1) rf_fft<N, E, false, false>(a, lbuf, t, tw);
       if constexpr (MODE == 2 || MODE == 3) {
 #pragma unroll
@@ -686,7 +708,10 @@ __global__ void __launch_bounds__(kThreads, (MODE >= 4 ? 1 : 2)) k_rstrided(Geom
       if constexpr (MODE != 0) rf_fft<N, E, true, false>(a, lbuf, t, tw);
       C* dst = Z.z[f0];
 #pragma unroll
-      for (int e = 0; e < E; ++e) dst[base + (t + T * e) * Su] = a[e];
+      for (int e = 0; e < E; ++e) {
+        if constexpr (REM) *rem(t + T * e) = a[e];
+        else dst[base + (t + T * e) * Su] = a[e];
+      }
     } else {
       C a[NF][E];
 #pragma unroll
@@ -1057,6 +1082,20 @@ static void rstrided_launch(const Geom& g, int axis, const ZList<C>& Z, int nin,
   count_launch();
 }
 
+template <int N, int EMAX, int MODE, typename C>
+static void rstrided_remote_launch(const Geom& gy, const RemoteZ& rz, int nin, const SpecOp& op, cudaStream_t st) {
+  constexpr int E = Ev<N, EMAX>::v, T = N / E;
+  int TXC = kThreads / T;
+  if (TXC > gy.nx) TXC = gy.nx;
+  const int threads = TXC * T;
+  const size_t sm = (size_t)TXC * RfCfg<N, E>::STRIDE * sizeof(C);
+  const long long items = (long long)(gy.nx / TXC) * gy.ny * nin;
+  const int blocks = persistent_blocks(k_rstrided<N, EMAX, MODE, C, true>, threads, sm, items);
+  ZList<C> Z{};
+  k_rstrided<N, EMAX, MODE, C, true><<<blocks, threads, sm, st>>>(gy, 2, TXC, nin, nin, Z, op, (int)items, rz);
+  count_launch();
+}
+
 #define TOPT_DISPATCH_N2(NV, BODY)                                  \
   switch (NV) {                                                     \
     case 8: { constexpr int N_ = 8; BODY; } break;                  \
@@ -1148,6 +1187,31 @@ void bchain_last(const Geom& gz, float2* const* Z, double alpha, int p, bool ler
   } else {
     TOPT_DISPATCH_N2(Nl, (rstrided_launch<N_, kE32, 3, float2>(gz, axis, L, nin, nout, op, st)));
   }
+}
+
+// z-slabs, P2P transport (3D, non-Leray): last-axis passes in place on the distributed slabs.
+// tab[f][q] = rank q's field f (z-slab layout), nzl planes per rank of plane_src elements.
+static RemoteZ make_rz(const void* const* tab, int nf, int P, int nzl, size_t plane_src) {
+  RemoteZ rz{};
+  int l = 0;
+  while ((1 << l) < nzl) ++l;
+  rz.lnzl = l;
+  rz.plane_src = (unsigned)plane_src;
+  for (int f = 0; f < nf && f < 4; ++f)
+    for (int q = 0; q < P && q < 8; ++q) rz.tab[f][q] = tab[f * P + q];
+  return rz;
+}
+void vchain_last_remote(const Geom& gy, const void* const* tab, int P, int nzl, size_t plane_src, double alpha, int p,
+                        double n_total, cudaStream_t st) {
+  const RemoteZ rz = make_rz(tab, vchain_nin(gy, false), P, nzl, plane_src);
+  SpecOp op{alpha, p, 1.0 / n_total};
+  TOPT_DISPATCH_N2(gy.nz, (rstrided_remote_launch<N_, kE64, 2, double2>(gy, rz, vchain_nin(gy, false), op, st)));
+}
+void bchain_last_remote(const Geom& gy, const void* const* tab, int P, int nzl, size_t plane_src, double alpha, int p,
+                        double n_total, cudaStream_t st) {
+  const RemoteZ rz = make_rz(tab, bchain_nin(gy, false), P, nzl, plane_src);
+  SpecOp op{alpha, p, 1.0 / n_total};
+  TOPT_DISPATCH_N2(gy.nz, (rstrided_remote_launch<N_, kE32, 3, float2>(gy, rz, bchain_nin(gy, false), op, st)));
 }
 
 // Merged last-axis pass (non-Leray): Zv (fp64 v spectra after x, y) and Zb (fp32 b
