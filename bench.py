@@ -251,8 +251,6 @@ def run_topt(args):
         try:
             t = topt.Topt(topt.Config(window=d["window"], **cfgp), device=dev, rank=rank, world=world,
                           unique_id=uid)
-            if args.transport == "p2p":
-                t.enable_p2p()
         except Exception as e:  # e.g. the NCCL communicator cannot be created on this node
             slab_error, err = f"{type(e).__name__}: {e}"[:200], 1.0
         if max_over_ranks(err, world, dev) > 0:  # every rank falls back together
@@ -260,6 +258,16 @@ def run_topt(args):
             slab_error = slab_error or "z-slab context failed on another rank"
             if rank == 0:
                 sys.stderr.write(f"bench: z-slab path unavailable ({slab_error}); running replicas\n")
+    if slab and args.transport == "p2p":  # CUDA IPC mapping of the peers' workspaces
+        perr = 0.0
+        try:
+            t.enable_p2p()
+        except Exception as e:
+            perr, slab_error = 1.0, f"p2p: {type(e).__name__}: {e}"[:200]
+        if max_over_ranks(perr, world, dev) > 0:  # every rank keeps the NCCL transport
+            t.set_transport("nccl")
+            args.transport = "nccl"
+            slab_error = slab_error or "p2p mapping failed on another rank"
     if slab:
         m0n, m1n = slab_of(d["m0"], rank, world), slab_of(d["m1"], rank, world)
         vn = slab_of(d["vstar"], rank, world, vector=True)
