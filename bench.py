@@ -184,6 +184,44 @@ def oracle_eval_rate(n_sample, device):
     return time.perf_counter() - t0, prob
 
 
+def oracle_stage_sample(cfg_n, device):
+    """The fp64 oracle (as it stands) timed at the FULL workload size on a bounded sample: one
+    instance of every stage of its evaluation (oracle.gradient.evaluate), each weighted by
+    how often one evaluation runs it (S = n_t): feet, the Heun factor (continuity), one forward and
+    one adjoint SL step (x S each), one body-force slice (x S+1), the gradient and preconditioner.
+    Returns (estimated seconds per evaluation, {stage: seconds})."""
+    from oracle import gradient as ogr
+    from oracle import spectral, transport
+    from oracle.interp import interp
+    from oracle.spectral import Grid
+    from synth import make_problem
+    import numba
+    numba.set_num_threads(_cpu_threads())
+    dw = make_problem(CONFIG, (16, 16, 16), device=device)  # JIT warm-up (not timed)
+    ogr.evaluate(ogr.Problem(Grid((16, 16, 16)), dw["m0"], dw["m1"], dw["alpha"], dw["nt"], dw["model"],
+                             dw["reg_order"]), dw["vstar"])
+    d = make_problem(CONFIG, cfg_n, device=device)
+    grid, S, v = Grid(tuple(d["n"])), d["nt"], d["vstar"]
+    t = {}
+
+    def clock(name, f):
+        t0 = time.perf_counter()
+        out = f()
+        t[name] = time.perf_counter() - t0
+        return out
+
+    df, da = clock("feet", lambda: transport.feet(grid, v, S))
+    E = clock("heun_factor", lambda: transport.source_factor_forward_continuity(grid, v, df, S))
+    m1 = clock("forward_step", lambda: interp(d["m0"], df) * E)
+    lam = clock("adjoint_step", lambda: interp(d["m1"] - m1, da))
+    clock("body_force_slice", lambda: -m1 * spectral.grad(grid, lam))
+    clock("gradient_precond", lambda: -spectral.apply_inv_alpha_L(
+        grid, d["alpha"] * spectral.apply_L(grid, v, d["reg_order"]), d["alpha"], d["reg_order"]))
+    count = {"feet": 1, "heun_factor": 1, "forward_step": S, "adjoint_step": S, "body_force_slice": S + 1,
+             "gradient_precond": 1}
+    return sum(t[k] * count[k] for k in t), t
+
+
 def run_reference(args):
     """--impl reference: the oracle as it stands on the host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -219,12 +257,15 @@ def run_reference(args):
     value = scale / sec
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True,
+        "sample_ms_per_step": sec * 1e3,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "config4_256^3_continuity_nt8_H2_alpha1e-3", "grid": [256, 256, 256]},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": _cpu_threads(), "kind": "oracle",
                          "sample": f"one fp64 oracle evaluation of the config-4 recipe at {n_s}^3 per step "
-                                   f"(rate scaled by ({n_s}/256)^3 to the 256^3 workload)"},
+                                   f"(sample_ms_per_step); value EXTRAPOLATED by ({n_s}/256)^3 to the 256^3 "
+                                   f"workload (ms_per_step = 1000 / value); bench.py's cpu_baseline times the "
+                                   f"oracle's stages at 256^3 itself"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -259,13 +300,11 @@ def run_topt(args):
             if rank == 0:
                 sys.stderr.write(f"bench: z-slab path unavailable ({slab_error}); running replicas\n")
     if slab and args.transport == "p2p":  # CUDA IPC mapping of the peers' workspaces
-        perr = 0.0
         try:
-            t.enable_p2p()
+            t.enable_p2p()  # collective: every rank ends on the same transport
         except Exception as e:
-            perr, slab_error = 1.0, f"p2p: {type(e).__name__}: {e}"[:200]
-        if max_over_ranks(perr, world, dev) > 0:  # every rank keeps the NCCL transport
-            t.set_transport("nccl")
+            slab_error = f"p2p: {type(e).__name__}: {e}"[:200]
+        if t.transport != "p2p":  # agreed over the ranks inside topt_set_transport
             args.transport = "nccl"
             slab_error = slab_error or "p2p mapping failed on another rank"
     if slab:
@@ -294,16 +333,18 @@ def run_topt(args):
         barrier()
         torch.cuda.synchronize()
         l0 = topt.Topt.launch_count()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        e0, e1 = ev[0], ev[-1]
         e0.record(stream)
-        for _ in range(args.steps):
+        for k in range(args.steps):  # one event per step boundary (no synchronisation inside)
             t.eval_gradient(m0, m1, v, g, s, sc)
-        e1.record(stream)
+            ev[k + 1].record(stream)
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
         launches = topt.Topt.launch_count() - l0
         ms = e0.elapsed_time(e1)
+        step_ms = sorted(ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps))
     ms = max_over_ranks(ms, world, dev)
     ms_per_step = ms / args.steps
     evals = args.steps if slab else world * args.steps  # slab: the ranks share one problem
@@ -397,8 +438,11 @@ def run_topt(args):
         if slab:  # a fresh NCCL unique id per communicator
             uid2 = share_unique_id(rank, world, topt.get_unique_id)
             ts = topt.Topt(topt.Config(**kw), device=dev, rank=rank, world=world, unique_id=uid2)
-            if args.transport == "p2p":
-                ts.enable_p2p()
+            if args.transport == "p2p":  # collective; falls back to NCCL on every rank together
+                try:
+                    ts.enable_p2p()
+                except Exception:
+                    pass
         else:
             ts = topt.Topt(topt.Config(**kw), device=dev)
         ts.solve(m0, m1)  # warm-up
@@ -425,11 +469,14 @@ def run_topt(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        sec, _ = oracle_eval_rate(args.cpu_n, str(dev))
-        scale = (args.cpu_n / d["n"][0]) ** 3
-        cpu = {"value": scale / sec, "unit": UNIT, "cores": _cpu_threads(), "kind": "oracle",
-               "sample": f"one fp64 oracle evaluation (oracle/, numba + numpy, as it stands) of the config-4 recipe "
-                         f"at {args.cpu_n}^3, rate scaled by ({args.cpu_n}/{d['n'][0]})^3 to the {d['n'][0]}^3 workload"}
+        del d
+        sec, stages = oracle_stage_sample(tuple(cfgp["n"]), str(dev))
+        cpu = {"value": 1.0 / sec, "unit": UNIT, "cores": _cpu_threads(), "kind": "oracle",
+               "sample": f"fp64 oracle (oracle/, numba + numpy, as it stands) on the {'x'.join(map(str, cfgp['n']))} "
+                         f"config-{args.config} workload itself: one instance of each evaluation stage timed, "
+                         f"weighted by its count per evaluation (S = {cfgp['nt']}): "
+                         + ", ".join(f"{k} {v:.2f} s" for k, v in stages.items()),
+               "sec_per_eval_estimated": round(sec, 3)}
 
     if rank == 0:
         wl = {1: "config1_2D_64^2_advection_nt4_H2", 2: "config2_64^3_advection_nt4_H1",
@@ -438,6 +485,10 @@ def run_topt(args):
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "step_ms": {"median": round(statistics.median(step_ms), 4),
+                        "p10": round(step_ms[int(0.1 * (len(step_ms) - 1))], 4),
+                        "p90": round(step_ms[int(round(0.9 * (len(step_ms) - 1)))], 4),
+                        "rank0_only": world > 1},
             "scaling": "strong" if slab else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": wl, "grid": list(d["n"]), "nt": d["nt"], "model": d["model"],
                        "reg_order": d["reg_order"], "alpha": d["alpha"],

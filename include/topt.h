@@ -47,7 +47,7 @@ typedef enum {
   TOPT_ERR_CUDA = -3,         /* a CUDA runtime error (message has the detail) */
   TOPT_ERR_NCCL = -4,         /* an NCCL error (world > 1) */
   TOPT_ERR_WORKSPACE = -5,    /* workspace missing or too small */
-  TOPT_ERR_HALO = -6          /* a characteristic foot leaves the halo of a z-slab */
+  TOPT_ERR_HALO = -6          /* internal: a foot left the sized z-slab window (never expected) */
 } topt_status;
 
 /* PDE constraint (P:35-41 advection; P:796-816 continuity; P:727-735 incompressible). */
@@ -154,13 +154,19 @@ topt_status topt_bind_workspace(topt_ctx* ctx, void* dptr, size_t bytes);
 topt_status topt_local_slab(const topt_ctx* ctx, int32_t* z0, int32_t* nz);
 
 /* z-slabs (world > 1): transport of the z<->y all-to-all transposes.
+ * COLLECTIVE with one process per GPU (every rank calls it, workspace bound; blocking): the
+ * transport set is 1 only if every rank asked for 1 and holds the peer mappings, else 0 on
+ * every rank — the ranks' collectives always match.
  * 0 (default) = pack + grouped ncclSend/ncclRecv + unpack; 1 = P2P pull: each rank reads its
  * chunks straight from the peers' slabs over NVLink (no pack / unpack passes), ordered by
  * one-byte all-reduce barriers.  With one process per GPU, transport 1 needs
- * topt_set_peer_workspaces first; with emulated slabs (one process) it runs the same pull
+ * topt_set_peer_workspaces first (topt_bind_workspace clears the mappings and resets 0); with emulated slabs (one process) it runs the same pull
  * kernel on the local slabs.  Transposes whose source is not in the workspace keep NCCL.
  * TOPT_ERR_INVALID_ARG for another value. */
 topt_status topt_set_transport(topt_ctx* ctx, int32_t transport);
+
+/* The transport in effect (0 or 1; -1 for a NULL context). */
+int32_t topt_get_transport(const topt_ctx* ctx);
 
 /* Peer workspaces for transport 1: bases[r] = rank r's bound workspace pointer (as passed to
  * its topt_bind_workspace) mapped into THIS process (CUDA IPC; bases[rank] = this rank's own),
@@ -173,9 +179,11 @@ topt_status topt_set_peer_workspaces(topt_ctx* ctx, void* const* bases, int32_t 
 /* GA-NGMRES(w; sigma, tau) (Alg. 3) or GA-AA from v^0 = v_inout (the
  * paper uses v^0 = 0).  m0, m1: F each; v_inout: d*F, overwritten with the
  * final iterate.  Synchronous (host decisions: Armijo, LSQ); report filled on exit.
- * z-slabs (world > 1): an Armijo trial whose characteristic foot leaves the 4-plane halo
- * (|delta_z| > 3 cells) is rejected like a failed Armijo test; an accepted iterate whose
- * foot does returns TOPT_ERR_HALO. */
+ * z-slabs (world > 1): every evaluation sizes its interpolation halo from the all-reduced
+ * max |v_z| dt/h (trace) and max |delta_z| (SL steps): feet with |delta_z| < 3 cells read the
+ * stored 4-plane halo, larger ones a window gathered from every slab they reach (up to a
+ * whole period, then wrapped), so no trial is rejected for halo reasons (SL: no CFL cap).
+ * TOPT_ERR_HALO would signal an internal error. */
 topt_status topt_solve(topt_ctx* ctx, const float* m0, const float* m1, float* v_inout,
                        topt_report* report, void* stream);
 

@@ -35,9 +35,26 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def _f32(t, device):
-    if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+def _f32(t, device, shape=None):
+    t = torch.as_tensor(t)
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ToptError(f"expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    if not (t.is_cuda and t.device == torch.device(device) and t.dtype == torch.float32 and t.is_contiguous()):
         t = t.to(device=device, dtype=torch.float32).contiguous()
+    return t
+
+
+def _out(t, shape, dtype, device=None, pinned=False, name="output"):
+    """Caller-supplied output buffer: the C ABI writes prod(shape) elements of `dtype` to it."""
+    if not isinstance(t, torch.Tensor):
+        raise ToptError(f"{name} must be a torch.Tensor")
+    if t.dtype != dtype or not t.is_contiguous() or t.numel() < int(torch.Size(shape).numel()):
+        raise ToptError(f"{name}: need a contiguous {dtype} tensor of >= {tuple(shape)} elements, got "
+                        f"{t.dtype} {tuple(t.shape)} contiguous={t.is_contiguous()}")
+    if device is not None and t.device != torch.device(device):
+        raise ToptError(f"{name} must live on {device}, not {t.device}")
+    if pinned and (t.is_cuda or not t.is_pinned()):
+        raise ToptError(f"{name} must be a pinned host tensor")
     return t
 
 
@@ -123,14 +140,26 @@ class Topt:
     def enable_p2p(self, group=None):
         """One process per GPU: map every rank's workspace into this process (CUDA IPC through
         torch's CUDA tensor sharing, handles exchanged with torch.distributed) and switch the
-        transposes to P2P pulls.  Collective: every rank calls it."""
-        maps, offs = map_peer_tensors(self.workspace, self.rank, self.world, self._ws_off, group)
-        self._peer_maps = maps  # keeps the mappings alive as long as this context
-        bases = (ctypes.c_void_p * self.world)()
-        for r in range(self.world):
-            bases[r] = maps[r].data_ptr() + offs[r]
-        check(LIB.topt_set_peer_workspaces(self.ctx, bases, self.world), "topt_set_peer_workspaces")
-        self.set_transport("p2p")
+        transposes to P2P pulls.  Collective: every rank calls it.  topt_set_transport agrees on the
+        transport over the ranks, so when the mapping fails on any rank every rank stays on NCCL
+        (this rank then re-raises the mapping error)."""
+        err = None
+        try:
+            maps, offs = map_peer_tensors(self.workspace, self.rank, self.world, self._ws_off, group)
+            self._peer_maps = maps  # keeps the mappings alive as long as this context
+            bases = (ctypes.c_void_p * self.world)()
+            for r in range(self.world):
+                bases[r] = maps[r].data_ptr() + offs[r]
+            check(LIB.topt_set_peer_workspaces(self.ctx, bases, self.world), "topt_set_peer_workspaces")
+        except Exception as e:  # noqa: BLE001 — re-raised after the collective below
+            err = e
+        self.set_transport("p2p")  # collective; p2p only if every rank holds its mappings
+        if err is not None:
+            raise err
+
+    @property
+    def transport(self) -> str:
+        return "p2p" if LIB.topt_get_transport(self.ctx) == 1 else "nccl"
 
     def __del__(self):
         try:
@@ -154,22 +183,34 @@ class Topt:
 
     # -- the benchmark unit
     def eval_gradient(self, m0, m1, v, g=None, s=None, scalars=None):
-        m0, m1, v = (_f32(x, self.device) for x in (m0, m1, v))
-        g = self._vec() if g is None else g
-        s = self._vec() if s is None else s
-        sc = self.scalars if scalars is None else scalars
+        m0, m1 = (_f32(x, self.device, self.shape) for x in (m0, m1))
+        v = _f32(v, self.device, (self.d,) + self.shape)
+        vshape = (self.d,) + self.shape
+        g = self._vec() if g is None else _out(g, vshape, torch.float32, self.device, name="g")
+        s = self._vec() if s is None else _out(s, vshape, torch.float32, self.device, name="s")
+        sc = self.scalars if scalars is None else _out(scalars, (_lib.NSCALARS,), torch.float64, self.device,
+                                                      name="scalars")
         check(LIB.topt_eval_gradient(self.ctx, _ptr(m0), _ptr(m1), _ptr(v), _ptr(g), _ptr(s), _ptr(sc),
                                      _stream()), "topt_eval_gradient")
         return g, s, sc
 
+    def _host_args(self, m0_h, m1_h, v_h, g_h, scal_h):
+        vshape = (self.d,) + self.shape
+        for name, x, shp in (("m0", m0_h, self.shape), ("m1", m1_h, self.shape), ("v", v_h, vshape),
+                             ("g", g_h, vshape)):
+            _out(x, shp, torch.float32, pinned=True, name=name)
+        _out(scal_h, (_lib.NSCALARS,), torch.float64, pinned=True, name="scalars")
+
     def eval_gradient_host(self, m0_h, m1_h, v_h, g_h, scal_h):
         """Host (pinned) buffers in, host buffers out; synchronous."""
+        self._host_args(m0_h, m1_h, v_h, g_h, scal_h)
         check(LIB.topt_eval_gradient_host(self.ctx, _ptr(m0_h), _ptr(m1_h), _ptr(v_h), _ptr(g_h),
                                           _ptr(scal_h), _stream()), "topt_eval_gradient_host")
 
     def eval_gradient_host_async(self, m0_h, m1_h, v_h, g_h, scal_h):
         """Host (pinned) buffers; enqueues and returns (results valid after the current
         stream is synchronised).  Consecutive calls overlap transfers with evaluation."""
+        self._host_args(m0_h, m1_h, v_h, g_h, scal_h)
         check(LIB.topt_eval_gradient_host_async(self.ctx, _ptr(m0_h), _ptr(m1_h), _ptr(v_h), _ptr(g_h),
                                                 _ptr(scal_h), _stream()), "topt_eval_gradient_host_async")
 

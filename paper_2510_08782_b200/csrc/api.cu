@@ -32,6 +32,8 @@ bool comm_allreduce(topt_ctx* c, const std::vector<double*>& ptr, int count, boo
 bool comm_p2p_ready(const topt_ctx* c);
 char* comm_peer(const topt_ctx* c, const void* p, int q);
 bool comm_fence(topt_ctx* c, cudaStream_t st);
+int comm_agree_min(topt_ctx* c, int v);
+bool comm_window(topt_ctx* c, const std::vector<const float*>& src, size_t fs, int nf, int zw, cudaStream_t st);
 }  // namespace topt
 
 namespace {
@@ -182,6 +184,8 @@ topt_status topt_create(const topt_params* p, int32_t rank, int32_t world, const
   }
   c->F = c->slabs[0].F;
   c->vecN = (size_t)c->d * c->F;
+  // window capacity: (nzl + 2 hcap) >= nz + 3 planes cover every periodic foot position
+  c->hcap = world > 1 ? (c->nzg - nzl + 4) / 2 : 0;
   // workspace size per slab
   const Slab& s0 = c->slabs[0];
   const size_t F = s0.F, Fh = s0.Fh, V = c->vecN, S1 = p->nt + 1, W1 = p->window + 1;
@@ -195,6 +199,7 @@ topt_status topt_create(const topt_params* p, int32_t rank, int32_t world, const
     add(4 * F * 8); add(3 * F * 16);                           // Zy, Zvy
     add(2 * S1 * F * 4); add(2 * F * 4);                       // ytraj, ytmp
     add(16 * F);                                               // sendbuf
+    add(3 * (F + 2 * (size_t)c->hcap * s0.plane) * 4);         // wide-halo window
   }
   add(F * 4); add(F * 4); add(V * 4); add(V * 4);              // m0b, m1b, vb, vt
   for (int i = 0; i < 12; ++i) add(V * 4);                     // solver vectors
@@ -266,6 +271,9 @@ topt_status topt_bind_workspace(topt_ctx* c, void* dptr, size_t bytes) {
   if (bytes < c->ws_need) return fail(TOPT_ERR_WORKSPACE, "workspace too small");
   c->ws = (char*)dptr;
   c->ws_bytes = bytes;
+  // peer mappings refer to the previous workspaces: transport 1 needs topt_set_peer_workspaces again
+  c->comm.peer_ws.clear();
+  c->comm.transport = 0;
   for (auto& ge : c->graphs) cudaGraphExecDestroy(ge.exec);  // they bake the old workspace in
   c->graphs.clear();
   const int world = c->world;
@@ -291,6 +299,7 @@ topt_status topt_bind_workspace(topt_ctx* c, void* dptr, size_t bytes) {
       sl.ytraj = (float*)take(2 * S1 * F * 4);
       sl.ytmp = (float*)take(2 * F * 4);
       sl.sendbuf = take(16 * F);
+      sl.win = (float*)take(3 * (F + 2 * (size_t)c->hcap * sl.plane) * 4);
     }
     sl.m0b = (float*)take(F * 4);
     sl.m1b = (float*)take(F * 4);
@@ -304,6 +313,8 @@ topt_status topt_bind_workspace(topt_ctx* c, void* dptr, size_t bytes) {
     sl.sc = (double*)take(5 * kSet * 8);
     sl.dots = (double*)take(kMaxVecs * kMaxVecs * 8);
     sl.haloerr = (int*)take(256);
+    sl.amax = (unsigned*)(sl.haloerr + 1);
+    sl.amaxd = (double*)sl.haloerr + 1;
     sl.g.haloerr = sl.haloerr;
     sl.gy.haloerr = sl.haloerr;
   }
@@ -314,9 +325,19 @@ topt_status topt_bind_workspace(topt_ctx* c, void* dptr, size_t bytes) {
 topt_status topt_set_transport(topt_ctx* ctx, int32_t transport) {
   if (!ctx) return fail(TOPT_ERR_INVALID_ARG, "NULL context");
   if (transport != 0 && transport != 1) return fail(TOPT_ERR_INVALID_ARG, "transport must be 0 or 1");
+  const Comm& cm = ctx->comm;
+  if (cm.P > 1 && !cm.emulated()) {
+    // collective: the ranks' choices decide which collectives each issues, so they must agree —
+    // transport 1 only if EVERY rank asked for it and holds the peer mappings
+    if (!ctx->ws) return fail(TOPT_ERR_WORKSPACE, "bind the workspace before topt_set_transport");
+    const int mine = transport == 1 && (int)cm.peer_ws.size() == cm.P ? 1 : 0;
+    transport = comm_agree_min(ctx, mine);
+  }
   ctx->comm.transport = transport;
   return TOPT_OK;
 }
+
+int32_t topt_get_transport(const topt_ctx* ctx) { return ctx ? ctx->comm.transport : -1; }
 
 topt_status topt_set_peer_workspaces(topt_ctx* ctx, void* const* bases, int32_t count) {
   if (!ctx) return fail(TOPT_ERR_INVALID_ARG, "NULL context");
@@ -451,6 +472,59 @@ bool halo(topt_ctx* c, std::function<float*(Slab&)> base, int nf, size_t fstride
   return comm_halo(c, b, nf, fstride, st);
 }
 
+// ---- z-slab window sizing ("halo exchange sized from max|v|*dt"; P:136 no CFL cap)
+// max |x| over every slab's F floats of a(slab) and b(slab) (b may be null), all-reduced (max),
+// on the host: synchronises `st` (z-slabs only; a few microseconds per evaluation)
+double zmax(topt_ctx* c, std::function<const float*(Slab&)> a, std::function<const float*(Slab&)> b,
+            cudaStream_t st) {
+  std::vector<double*> slots;
+  for (auto& sl : c->slabs) {
+    cudaMemsetAsync(sl.amax, 0, sizeof(unsigned), st);
+    launch_absmax(a(sl), b ? b(sl) : nullptr, sl.F, sl.amax, st);
+    launch_uint_as_float_to_double(sl.amax, sl.amaxd, st);
+    slots.push_back(sl.amaxd);
+  }
+  comm_allreduce(c, slots, 1, true, st);
+  double h = 0.0;
+  cudaMemcpyAsync(&h, c->slabs[0].amaxd, sizeof(double), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  return h;
+}
+// Half-width of the input window for feet of at most D cells in z: the tricubic stencil of a
+// foot z + delta spans planes floor(z + delta) - 1 .. + 2, so |delta| <= D needs floor(D) + 2
+// planes per side.  0 = the stored kSlabHalo planes suffice (D < 3); beyond the capacity the
+// window covers a whole period and feet are wrapped into it (nzw).
+void size_window(const topt_ctx* c, double D, int& zw, bool& wrap) {
+  const double need = std::isfinite(D) ? std::floor(D * (1.0 + 1e-6)) + 2.0 : 1e30;
+  if (need <= kSlabHalo) {
+    zw = 0;
+    wrap = false;
+    return;
+  }
+  zw = (int)std::min<double>(need, c->hcap);
+  wrap = need > c->hcap;
+}
+Geom in_geom(const topt_ctx* c, const Slab& sl, int zw, bool wrap) {
+  if (!zw) return sl.g;
+  Geom g = sl.g;
+  g.zh = zw;
+  g.nzw = wrap ? c->nzg : 0;
+  return g;
+}
+// Input of an interpolation over nf fields (field f of slab s at base(s) + f * fstride, halo'd
+// layout): the stored halo refreshed (zw == 0) or the window gathered into s.win from the LOCAL
+// planes of every slab (multi-hop).  The kernel then reads in_ptr(...) with in_geom(...).
+bool sl_input(topt_ctx* c, std::function<float*(Slab&)> base, int nf, size_t fstride, int zw, cudaStream_t st) {
+  if (P_of(c) == 1) return true;
+  if (zw == 0) return halo(c, base, nf, fstride, st);
+  std::vector<const float*> src;
+  for (auto& sl : c->slabs) src.push_back(local(sl, base(sl)));
+  const Slab& s0 = c->slabs[0];
+  Prof pr(c, K_COMM, 2.0 * nf * (s0.F + 2.0 * zw * s0.plane) * 4.0 * c->comm.nloc, 0, st);
+  return comm_window(c, src, fstride, nf, zw, st);
+}
+const float* in_ptr(const Slab& sl, const float* base, int zw) { return zw ? sl.win : base; }
+
 // div v = sum_a d_a v_a (R3), into the local planes of divv; halo refreshed
 void compute_div(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
   const int P = P_of(c);
@@ -579,19 +653,31 @@ void forward_half(topt_ctx* c, std::vector<Io>& io, bool want_adj, cudaStream_t 
       for (int a = 0; a < c->d; ++a)
         cudaMemcpyAsync(local(sl, sl.vh + a * sl.Fh), io[si].v + a * sl.F, sl.F * 4, cudaMemcpyDeviceToDevice, st);
     }
-    halo(c, [](Slab& s) { return s.vh; }, c->d, c->slabs[0].Fh, st);
+    // trace input: midpoint displacements dt/2 v_z/h_z at the nodes (exact, no interpolation)
+    const double Dv = 0.5 * zmax(c, [](Slab& s) { return (const float*)local(s, s.vh + 2 * s.Fh); }, nullptr, st) *
+                      (double)c->slabs[0].g.cz;
+    size_window(c, Dv, c->zw_v, c->wrap_v);
+    sl_input(c, [](Slab& s) { return s.vh; }, c->d, c->slabs[0].Fh, c->zw_v, st);
   }
   for (size_t si = 0; si < c->slabs.size(); ++si) {
     Slab& sl = c->slabs[si];
     int np = 0;
     {
       Prof pr(c, K_TRACE, (d + d * (want_adj ? 2 : 1)) * F4, 1, st);
-      launch_trace(sl.g, P > 1 ? sl.vh : io[si].v, sl.df, want_adj ? sl.da : nullptr, sl.partials, &np, st);
+      launch_trace(in_geom(c, sl, c->zw_v, c->wrap_v), P > 1 ? in_ptr(sl, sl.vh, c->zw_v) : io[si].v, sl.df,
+                   want_adj ? sl.da : nullptr, sl.partials, &np, st);
     }
     Prof pr(c, K_MISC, 0.0, 1, st);
     launch_finalize_slots(sl.partials, 0, c->d, np, false, io[si].isc + I_SUMV, st);
   }
   comm_allreduce(c, intls(io, I_SUMV), c->d, false, st);
+  if (P > 1) {  // SL-step inputs: max |delta_z| over both feet
+    const double D = zmax(c, [](Slab& s) { return (const float*)s.df + 2 * s.F; },
+                          want_adj ? std::function<const float*(Slab&)>([](Slab& s) { return (const float*)s.da + 2 * s.F; })
+                                   : std::function<const float*(Slab&)>(), st);
+    size_window(c, D, c->zw_m, c->wrap_m);
+  }
+  const int zw = c->zw_m;
   const bool cont = c->p.model == TOPT_CONTINUITY;
   if (cont) {
     if (c->div_pending) {
@@ -601,9 +687,11 @@ void forward_half(topt_ctx* c, std::vector<Io>& io, bool want_adj, cudaStream_t 
       Prof pr(c, K_DIV, (3.0 * d - 1.0) * F4, c->d, st);
       compute_div(c, io, st);
     }
+    if (zw) sl_input(c, [](Slab& s) { return s.divv; }, 1, 0, zw, st);
     for (auto& sl : c->slabs) {
       Prof pr(c, K_EFACTOR, (d + 2) * F4, 1, st);
-      launch_efactor(sl.g, sl.divv, sl.df, (float)(-0.5 * c->dt), (float)(0.5 * c->dt * c->dt), sl.E, st);
+      launch_efactor(in_geom(c, sl, zw, c->wrap_m), in_ptr(sl, sl.divv, zw), sl.df, (float)(-0.5 * c->dt),
+                     (float)(0.5 * c->dt * c->dt), sl.E, st);
     }
   }
   const double e = cont ? 1.0 : 0.0;
@@ -614,16 +702,18 @@ void forward_half(topt_ctx* c, std::vector<Io>& io, bool want_adj, cudaStream_t 
   }
   std::vector<int> np(c->slabs.size(), 0);
   for (int j = 0; j < S; ++j) {
-    halo(c, [j](Slab& s) { return s.m_traj + j * s.Fh; }, 1, 0, st);
+    sl_input(c, [j](Slab& s) { return s.m_traj + j * s.Fh; }, 1, 0, zw, st);
     for (size_t si = 0; si < c->slabs.size(); ++si) {
       Slab& sl = c->slabs[si];
       const float* Ef = cont ? sl.E : nullptr;
+      const Geom gi = in_geom(c, sl, zw, c->wrap_m);
+      const float* in = in_ptr(sl, sl.m_traj + j * sl.Fh, zw);
       if (j + 1 < S) {
         Prof pr(c, K_SL_STEP, (d + 2 + e) * F4, 1, st);
-        launch_sl_step(sl.g, sl.m_traj + j * sl.Fh, sl.df, Ef, local(sl, sl.m_traj + (j + 1) * sl.Fh), st);
+        launch_sl_step(gi, in, sl.df, Ef, local(sl, sl.m_traj + (j + 1) * sl.Fh), st);
       } else {
         Prof pr(c, K_SL_LAST, (d + 4 + e) * F4, 1, st);
-        launch_sl_last(sl.g, sl.m_traj + j * sl.Fh, sl.df, Ef, io[si].m1, local(sl, sl.m_traj + S * sl.Fh),
+        launch_sl_last(gi, in, sl.df, Ef, io[si].m1, local(sl, sl.m_traj + S * sl.Fh),
                        local(sl, sl.lam_traj + S * sl.Fh), sl.partials, &np[si], st);
       }
     }
@@ -644,6 +734,7 @@ void backward_half(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
   const size_t F = c->F;
   const double F4 = 4.0 * F, d = c->d;
   const bool adv = c->p.model == TOPT_ADVECTION;
+  const int zw = c->zw_m;  // sized by forward_half from both feet
   if (adv) {
     if (c->div_pending) {
       cudaStreamWaitEvent(st, c->ev_div, 0);
@@ -652,18 +743,20 @@ void backward_half(topt_ctx* c, std::vector<Io>& io, cudaStream_t st) {
       Prof pr(c, K_DIV, (3.0 * d - 1.0) * F4, c->d, st);
       compute_div(c, io, st);
     }
+    if (zw) sl_input(c, [](Slab& s) { return s.divv; }, 1, 0, zw, st);
     for (auto& sl : c->slabs) {
       Prof pr(c, K_EFACTOR, (d + 2) * F4, 1, st);
-      launch_efactor(sl.g, sl.divv, sl.da, (float)(0.5 * c->dt), (float)(0.5 * c->dt * c->dt), sl.E, st);
+      launch_efactor(in_geom(c, sl, zw, c->wrap_m), in_ptr(sl, sl.divv, zw), sl.da, (float)(0.5 * c->dt),
+                     (float)(0.5 * c->dt * c->dt), sl.E, st);
     }
   }
   const double e = adv ? 1.0 : 0.0;
   for (int j = S - 1; j >= 0; --j) {
-    halo(c, [j](Slab& s) { return s.lam_traj + (j + 1) * s.Fh; }, 1, 0, st);
+    sl_input(c, [j](Slab& s) { return s.lam_traj + (j + 1) * s.Fh; }, 1, 0, zw, st);
     for (auto& sl : c->slabs) {
       Prof pr(c, K_SL_STEP, (d + 2 + e) * F4, 1, st);
-      launch_sl_step(sl.g, sl.lam_traj + (j + 1) * sl.Fh, sl.da, adv ? sl.E : nullptr,
-                     local(sl, sl.lam_traj + j * sl.Fh), st);
+      launch_sl_step(in_geom(c, sl, zw, c->wrap_m), in_ptr(sl, sl.lam_traj + (j + 1) * sl.Fh, zw), sl.da,
+                     adv ? sl.E : nullptr, local(sl, sl.lam_traj + j * sl.Fh), st);
     }
   }
   // body force
@@ -941,7 +1034,7 @@ topt_status fetch(topt_ctx* c, int set, HostScalars& out, cudaStream_t st) {
   TOPT_CUDA(cudaMemcpyAsync(out.v, c->slabs[0].sc + set * kSet, sizeof(out.v), cudaMemcpyDeviceToHost, st));
   TOPT_CUDA(cudaStreamSynchronize(st));
   if (c->comm.P > 1 && out.v[kSet - 1] != 0.0)
-    return fail(TOPT_ERR_HALO, "a characteristic foot left the z-slab halo (|delta_z| > 3 cells)");
+    return fail(TOPT_ERR_HALO, "internal: a characteristic foot left the sized z-slab window");
   return TOPT_OK;
 }
 
@@ -1634,13 +1727,7 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
         if ((r = graphs_ok(c) ? graph_run(c, key, st, body) : body(st)) != TOPT_OK) return r;
         ++obj_evals;
         HostScalars ts;
-        r = fetch(c, 1, ts, st);
-        if (r == TOPT_ERR_HALO) {  // trial foot beyond the z-slab halo: reject the trial, backtrack
-          for (auto& sl : c->slabs) TOPT_CUDA(cudaMemsetAsync(sl.haloerr, 0, sizeof(int), st));
-          rho_t *= 0.5;
-          continue;
-        }
-        if (r != TOPT_OK) return r;
+        if ((r = fetch(c, 1, ts, st)) != TOPT_OK) return r;
         // reg(v + rho s) = reg + rho alpha<s, L v> + rho^2/2 alpha<s, L s>  (exact: quadratic)
         const double reg_t = cur.pub(TOPT_S_REG) + rho_t * cur.pub(TOPT_S_SLV) +
                              0.5 * rho_t * rho_t * cur.pub(TOPT_S_SLS);

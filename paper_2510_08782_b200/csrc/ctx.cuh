@@ -2,7 +2,11 @@
 //
 // z-slab decomposition (BASELINE north_star): the 3D grid is cut into P slabs of
 // nz/P planes.  Each slab owns its fields; interpolated inputs carry zh = 4 halo planes per
-// side (ring-periodic neighbour exchange before every SL step), z-derivatives and the z passes
+// side (ring-periodic neighbour exchange before every SL step) — enough for feet with
+// |delta_z| < 3 cells.  The halo is sized per evaluation from the all-reduced max |v_z| dt/h
+// (trace) and max |delta_z| (SL steps): when a foot needs more, the step's input is gathered
+// into a wider window (multi-hop: planes from every slab they live on, up to a whole period),
+// so no foot is ever out of reach (SL has no CFL limit); z-derivatives and the z passes
 // of the 3D FFTs run in a y-slab layout [nz][ny/P][nx] reached by an all-to-all transpose, and
 // reductions are all-reduced.  One process may hold every slab (emulation on one GPU: the
 // exchanges are device copies — used to test P-invariance) or exactly one (NCCL over NVLink).
@@ -47,6 +51,9 @@ struct Slab {
   double* sc{};    // 5 sets of kSet
   double* dots{};
   int* haloerr{};
+  unsigned* amax{};  // max |x| as float bits (window sizing)
+  double* amaxd{};   // the same as a double (all-reduced)
+  float* win{};      // wide-halo window: 3 fields of (nz + 2 hcap) planes
   double* pub(int set) const { return sc + set * kSet; }
   double* intl(int set) const { return sc + set * kSet + 16; }
 };
@@ -82,6 +89,11 @@ struct topt_ctx {
   topt::Comm comm;
   std::vector<topt::Slab> slabs;
   std::vector<double> replay;
+  // z-slab window sizing (P > 1): capacity hcap (covers a whole period), and the half-widths of
+  // this evaluation's trace input (zw_v) and SL-step inputs (zw_m); 0 = the stored 4-plane halo
+  int hcap = 0;
+  int zw_v = 0, zw_m = 0;
+  bool wrap_v = false, wrap_m = false;
   // side stream for work that depends on v only (eval_gradient, single slab)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_div = nullptr, ev_u = nullptr;

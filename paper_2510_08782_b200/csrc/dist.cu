@@ -171,6 +171,70 @@ bool comm_halo(topt_ctx* c, const std::vector<float*>& base, int nf, size_t fstr
 #endif
 }
 
+// Wide-halo window (multi-hop): slab r's window plane w (w < nzl + 2 zw) is global plane
+// (z0_r - zw + w) mod nz, copied from the slab that owns it — up to every slab when zw > nzl.
+// nf fields: field f of slab s at src[s] + f * fs floats (its LOCAL planes), written to slab s's
+// win + f * (nzl + 2 zw) plane floats.  Runs of consecutive planes with one owner move as one
+// copy (emulated) or one ncclSend / ncclRecv pair, issued in window order on both sides.
+namespace {
+struct Run { int q, lp, w, len; };
+std::vector<Run> window_runs(int z0, int nzl, int nzg, int zw) {
+  std::vector<Run> runs;
+  const int W = nzl + 2 * zw;
+  for (int w = 0; w < W;) {
+    int zg = (z0 - zw + w) % nzg;
+    if (zg < 0) zg += nzg;
+    const int q = zg / nzl, lp = zg - q * nzl, len = std::min(W - w, nzl - lp);
+    runs.push_back({q, lp, w, len});
+    w += len;
+  }
+  return runs;
+}
+}  // namespace
+
+bool comm_window(topt_ctx* c, const std::vector<const float*>& src, size_t fs, int nf, int zw, cudaStream_t st) {
+  const Comm& cm = c->comm;
+  const Slab& s0 = c->slabs[0];
+  const int nzl = s0.g.nz, nzg = nzl * cm.P;
+  const size_t pl = s0.plane, ws = (size_t)(nzl + 2 * zw) * pl;
+  if (zw > c->hcap) return false;
+  if (cm.emulated()) {
+    for (int r = 0; r < cm.P; ++r)
+      for (const Run& u : window_runs(r * nzl, nzl, nzg, zw))
+        for (int f = 0; f < nf; ++f)
+          cudaMemcpyAsync(c->slabs[r].win + f * ws + (size_t)u.w * pl, src[u.q] + f * fs + (size_t)u.lp * pl,
+                          (size_t)u.len * pl * 4, cudaMemcpyDeviceToDevice, st);
+    return cudaGetLastError() == cudaSuccess;
+  }
+#ifdef TOPT_WITH_NCCL
+  const int me = s0.index;
+  float* win = c->slabs[0].win;
+  for (const Run& u : window_runs(me * nzl, nzl, nzg, zw))  // my own planes
+    if (u.q == me)
+      for (int f = 0; f < nf; ++f)
+        cudaMemcpyAsync(win + f * ws + (size_t)u.w * pl, src[0] + f * fs + (size_t)u.lp * pl, (size_t)u.len * pl * 4,
+                        cudaMemcpyDeviceToDevice, st);
+  bool ok = nccl_ok(ncclGroupStart(), "ncclGroupStart");
+  for (int r = 0; r < cm.P && ok; ++r) {
+    if (r == me) continue;
+    for (const Run& u : window_runs(r * nzl, nzl, nzg, zw))  // what rank r needs from me
+      if (u.q == me)
+        for (int f = 0; f < nf; ++f)
+          ok &= nccl_ok(ncclSend(src[0] + f * fs + (size_t)u.lp * pl, (size_t)u.len * pl * 4, ncclChar, r, cm.nccl, st),
+                        "ncclSend");
+  }
+  for (const Run& u : window_runs(me * nzl, nzl, nzg, zw))  // what I need from the others
+    if (u.q != me)
+      for (int f = 0; f < nf && ok; ++f)
+        ok &= nccl_ok(ncclRecv(win + f * ws + (size_t)u.w * pl, (size_t)u.len * pl * 4, ncclChar, u.q, cm.nccl, st),
+                      "ncclRecv");
+  ok &= nccl_ok(ncclGroupEnd(), "ncclGroupEnd");
+  return ok && cudaGetLastError() == cudaSuccess;
+#else
+  return false;
+#endif
+}
+
 // z-slab -> y-slab transpose of one field per slab (element size eb bytes).
 bool comm_z2y(topt_ctx* c, const std::vector<const char*>& src, const std::vector<char*>& dst, size_t eb,
               cudaStream_t st) {
@@ -228,6 +292,27 @@ bool comm_y2z(topt_ctx* c, const std::vector<const char*>& src, const std::vecto
   return ok;
 #else
   return false;
+#endif
+}
+
+// Collective agreement (one process per GPU): the minimum of `v` over the ranks, through the
+// slab's scratch word (workspace bound), blocking.  Emulated / single slab: v itself.
+int comm_agree_min(topt_ctx* c, int v) {
+  const Comm& cm = c->comm;
+  if (cm.P == 1 || cm.emulated()) return v;
+#ifdef TOPT_WITH_NCCL
+  int* d = reinterpret_cast<int*>(c->slabs[0].amax);
+  cudaStream_t st;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return 0;
+  int out = 0;
+  cudaMemcpyAsync(d, &v, sizeof(int), cudaMemcpyHostToDevice, st);
+  const bool ok = nccl_ok(ncclAllReduce(d, d, 1, ncclInt32, ncclMin, cm.nccl, st), "ncclAllReduce(agree)");
+  cudaMemcpyAsync(&out, d, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  return ok ? out : 0;
+#else
+  return 0;
 #endif
 }
 

@@ -27,6 +27,10 @@ struct Geom {
   // y-slab geometry of the z passes: global y offset of local row 0 and global ny (0 = local)
   int ky0, nyg;
   int* haloerr;     // device flag: set to 1 when a foot leaves the halo (zh > 0)
+  // window path (zh > the stored halo): when nonzero, the z period of the global grid — the
+  // window [zh + nz + zh] planes covers every periodic position (zh >= (nzw - nz + 3) / 2), so a
+  // foot outside it is wrapped by multiples of nzw into it (any CFL)
+  int nzw;
 };
 
 // Reduction helper: per-block fp64 partials, finalised in fixed order.
@@ -153,6 +157,10 @@ void launch_multidot(const float* a, const float* const* bs, int count, size_t n
                      int* nparts, cudaStream_t st);
 void launch_mix(const float* q, const float* const* vs, const double* beta, int count, size_t n,
                 float* out, cudaStream_t st);
+// *acc = max(*acc, bits of max |x|) over x = a[0..n) and b[0..n) (b may be null); non-negative floats
+// order like their bit patterns, so the running maximum is an atomicMax on unsigned (caller zeroes it)
+void launch_absmax(const float* a, const float* b, size_t n, unsigned* acc, cudaStream_t st);
+void launch_uint_as_float_to_double(const unsigned* acc, double* d, cudaStream_t st);
 void launch_axpy(const float* x, float a, const float* y, size_t n, float* out, cudaStream_t st);  // out = x + a*y
 void launch_sub(const float* a, const float* b, size_t n, float* out, cudaStream_t st);           // out = a - b
 void launch_axpy_c(const float* x, float a, const float* y, size_t n, int ncomp, const float* cst, float* out,

@@ -80,10 +80,17 @@ __device__ __forceinline__ T* at_u32(T* base, unsigned idx) {
 __device__ __forceinline__ float gather_global(const Geom& g, const float* __restrict__ f, int x, int y, int z,
                                                float dx, float dy, float dz) {
   const float fx = floorf(dx), fy = floorf(dy), fz = floorf(dz);
-  const int ix = x + (int)fx, iy = y + (int)fy, iz = z + (int)fz;
-  if (g.zh && (iz - 1 < -g.zh || iz + 2 >= g.nz + g.zh)) {  // foot beyond the neighbour's halo
-    if (g.haloerr) *g.haloerr = 1;
-    return 0.0f;
+  const int ix = x + (int)fx, iy = y + (int)fy;
+  int iz = z + (int)fz;
+  if (g.zh && (iz - 1 < -g.zh || iz + 2 >= g.nz + g.zh)) {  // foot beyond the slab's halo / window
+    if (!g.nzw) {
+      if (g.haloerr) *g.haloerr = 1;  // the host sizes the window from max |delta_z|: never reached
+      return 0.0f;
+    }
+    // the window covers a whole period: wrap iz into [-zh + 1, nzw - zh] (periodic in z)
+    int r = (iz + g.zh - 1) % g.nzw;
+    if (r < 0) r += g.nzw;
+    iz = r - g.zh + 1;
   }
   float wx[4], wy[4], wz[4];
   lag4(dx - fx, wx);

@@ -315,6 +315,7 @@ __global__ void __launch_bounds__(kThreads, (EMAX == 8 || N == 256 ? TOPT_RDS16_
       *reinterpret_cast<float2*>(sos[zr >> lnzl] + (zr & zmask) * plane_src + yx) = acc[e];
     }
   }
+  __threadfence_system();  // the b_z stores into the peers' slabs, before the barrier that follows
 }
 
 static int ilog2i(int n) {
@@ -782,6 +783,8 @@ __global__ void __launch_bounds__(kThreads, (MODE >= 4 ? 1 : 2)) k_rstrided(Geom
       }
     }
   }
+  // remote (peer) stores: visible system-wide before the stream-ordered barrier that follows
+  if constexpr (REM) __threadfence_system();
 }
 
 // Merged last-axis pass of the v- and b-chains (non-Leray): the forward transform of the

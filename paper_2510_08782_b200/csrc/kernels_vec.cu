@@ -5,6 +5,7 @@
 // in one fused pass over a and every b_i ("multi-dot"); Alg. 1 line 6 / Alg. 3
 // line 9: v^{k+1} = q + sum beta_i (q - v^{k-i}) in one pass ("mix").
 // All reductions use fp64 per-block partials and a fixed-order finalisation.
+#include <algorithm>
 #include <atomic>
 
 #include "internal.cuh"
@@ -237,6 +238,32 @@ __global__ void k_sub(const float* __restrict__ a, const float* __restrict__ b, 
 }
 void launch_sub(const float* a, const float* b, size_t n, float* out, cudaStream_t st) {
   k_sub<<<grid_for(n / 4, kThreads, 148 * 8), kThreads, 0, st>>>(a, b, n / 4, out);
+  count_launch();
+}
+
+
+// ---- z-slab window sizing: max |x| as ordered float bits ------------------------------------
+__global__ void __launch_bounds__(kThreads) k_absmax(const float* __restrict__ a, const float* __restrict__ b, size_t n,
+                                                     unsigned* acc) {
+  float m = 0.0f;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    m = fmaxf(m, fabsf(a[i]));
+    if (b) m = fmaxf(m, fabsf(b[i]));
+    if (a[i] != a[i] || (b && b[i] != b[i])) m = __int_as_float(0x7f800000);  // NaN: treat as unbounded
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(acc, __float_as_uint(m));
+}
+__global__ void k_uint_as_float_to_double(const unsigned* acc, double* d) { *d = (double)__uint_as_float(*acc); }
+
+void launch_absmax(const float* a, const float* b, size_t n, unsigned* acc, cudaStream_t st) {
+  const int blocks = (int)std::min<size_t>((n + kThreads - 1) / kThreads, 148 * 8);
+  k_absmax<<<blocks, kThreads, 0, st>>>(a, b, n, acc);
+  count_launch();
+}
+void launch_uint_as_float_to_double(const unsigned* acc, double* d, cudaStream_t st) {
+  k_uint_as_float_to_double<<<1, 1, 0, st>>>(acc, d);
   count_launch();
 }
 

@@ -36,9 +36,8 @@ def test_smallest_grids(cfg, n, model):
     t = topt_for(d)
     g, s, sc = t.eval_gradient(dev(d["m0"]), dev(d["m1"]), dev(d["v"]))
     ref = ogr.evaluate(d["prob"], d["v"])
-    kappa = max(1.0, np.linalg.norm(ref["m"][-1]) / np.linalg.norm(ref["lam"][-1]))
-    assert rel_l2(host(g), ref["g"]) < TOL * kappa
-    assert rel_l2(host(s), ref["s"]) < TOL * kappa
+    assert rel_l2(host(g), ref["g"]) < TOL
+    assert rel_l2(host(s), ref["s"]) < TOL
     assert abs(t.scalars_dict(sc)["obj"] - ref["obj"]) <= TOL * abs(ref["obj"])
 
 
@@ -48,8 +47,7 @@ def test_few_time_steps(nt):
     t = topt_for(d)
     g, s, sc = t.eval_gradient(dev(d["m0"]), dev(d["m1"]), dev(d["v"]))
     ref = ogr.evaluate(d["prob"], d["v"])
-    kappa = max(1.0, np.linalg.norm(ref["m"][-1]) / np.linalg.norm(ref["lam"][-1]))
-    assert rel_l2(host(g), ref["g"]) < TOL * kappa
+    assert rel_l2(host(g), ref["g"]) < TOL
     assert abs(t.scalars_dict(sc)["obj"] - ref["obj"]) <= TOL * abs(ref["obj"])
 
 
@@ -63,8 +61,7 @@ def test_h1_h3_regularisers(p, model):
     t = topt_for(d)
     g, s, sc = t.eval_gradient(dev(d["m0"]), dev(d["m1"]), dev(d["v"]))
     ref = ogr.evaluate(d["prob"], d["v"])
-    kappa = max(1.0, np.linalg.norm(ref["m"][-1]) / np.linalg.norm(ref["lam"][-1]))
-    assert rel_l2(host(g), ref["g"]) < TOL * kappa
+    assert rel_l2(host(g), ref["g"]) < TOL
     assert rel_l2(host(s), ref["s"]) < TOL
     sd = t.scalars_dict(sc)
     assert abs(sd["reg"] - ref["reg"]) <= TOL * abs(ref["reg"])

@@ -76,31 +76,58 @@ def test_precond_and_leray(cfg, n, model):
     assert rel_l2(pl, spectral.leray(d["grid"], g)) < TOL
 
 
+def _propagated(d, ref, lamS_gpu):
+    """The oracle's own adjoint + body force + gradient applied to the GPU's fp32 lam^S instead of
+    its own: what the forward sweep's admissible error becomes downstream."""
+    grid, nt, v, model = d["grid"], d["nt"], d["v"], d["model"]
+    E = ref["E"] if model == 0 else None
+    lam = transport.adjoint(lamS_gpu, ref["delta_a"], nt, E)
+    w = ogr.trapezoid_weights(nt)
+    b = np.zeros_like(ref["b"])
+    for j in range(nt + 1):
+        if model == 1:
+            b -= w[j] * ref["m"][j] * spectral.grad(grid, lam[j])
+        else:
+            b += w[j] * lam[j] * spectral.grad(grid, ref["m"][j])
+    g = d["alpha"] * spectral.apply_L(grid, v, d["reg_order"]) + b
+    if model == 2:
+        g = spectral.leray(grid, g)
+    return lam, b, g
+
+
 @pytest.mark.parametrize("cfg,n", GRIDS)
 @pytest.mark.parametrize("model", [0, 1, 2])
 def test_eval_gradient(cfg, n, model):
-    """Whole evaluation.  The adjoint starts from the mismatch lam^S = m1 - m^S (R1), whose relative
-    error is the forward sweep's (<= 1e-5 of ||m^S||) times kappa = ||m^S|| / ||m1 - m^S||; lam, b
-    and g are therefore held to TOL * max(1, kappa), everything else to TOL."""
+    """Whole evaluation end to end against the oracle's whole evaluation.  Everything is held to the
+    bare tolerance TOL, except that lam^j, b and g may in addition carry the forward sweep's error
+    propagated through the (linear) adjoint / body-force / gradient maps, computed here exactly by
+    the oracle from the GPU's lam^S (lam^S = m1 - m^S cancels, amplifying the
+    forward error by kappa = ||m^S|| / ||m1 - m^S||, 10.2 on the 32 x 16 x 64 grid).  The forward
+    error itself, and each operator on its own (tests/test_gpu_operators.py), are held to TOL."""
     d = case(cfg, n, model=model)
     if model == 2:
         d["v"] = spectral.leray(d["grid"], d["v"]).astype(np.float32).astype(np.float64)
     t = topt_for(d)
     g, s, sc = t.eval_gradient(dev(d["m0"]), dev(d["m1"]), dev(d["v"]))
     ref = ogr.evaluate(d["prob"], d["v"])
-    kappa = max(1.0, np.linalg.norm(ref["m"][-1]) / np.linalg.norm(ref["lam"][-1]))
-    tol_adj = TOL * kappa
     lam, b = t.adjoint()
-    lam, b = host(lam), host(b)
-    for j in range(d["nt"] + 1):
-        assert rel_l2(lam[j], ref["lam"][j]) < tol_adj, ("lam", j)
-    assert rel_l2(b, ref["b"]) < tol_adj, "b"
-    assert rel_l2(host(g), ref["g"]) < tol_adj, "g"
-    assert rel_l2(host(s), ref["s"]) < TOL, "s"
+    lam, b, g, s = host(lam), host(b), host(g), host(s)
+    nt = d["nt"]
+    m = host(t.forward(dev(d["m0"]), dev(d["v"])))
+    errs = {f"m{j}": rel_l2(m[j], ref["m"][j]) for j in range(nt + 1)}
+    plam, pb, pg = _propagated(d, ref, lam[nt])
+    allow = {}
+    for j in range(nt + 1):
+        errs[f"lam{j}"] = rel_l2(lam[j], ref["lam"][j])
+        allow[f"lam{j}"] = rel_l2(plam[j], ref["lam"][j])
+    errs.update(b=rel_l2(b, ref["b"]), g=rel_l2(g, ref["g"]), s=rel_l2(s, ref["s"]))
+    allow.update(b=rel_l2(pb, ref["b"]), g=rel_l2(pg, ref["g"]))
     sd = t.scalars_dict(sc)
-    for k in ("obj", "dist", "reg", "gs"):
-        assert abs(sd[k] - ref[k]) <= TOL * abs(ref[k]) + 1e-30, k
-    assert abs(sd["grad_inf"] - ref["grad_inf"]) <= tol_adj * ref["grad_inf"]
+    for k in ("obj", "dist", "reg", "gs", "grad_inf"):
+        errs[k] = abs(sd[k] - ref[k]) / (abs(ref[k]) + 1e-300)
+    print(cfg, n, model, {k: f"{e:.2e}" + (f"/{allow[k]:.1e}" if k in allow else "") for k, e in errs.items()})
+    bad = {k: e for k, e in errs.items() if not e < TOL + allow.get(k, 0.0)}
+    assert not bad, bad
 
 
 def test_multidot_and_mix():
@@ -120,18 +147,21 @@ def test_multidot_and_mix():
 
 def test_underresolved_grid_conditioning():
     """Config-5 recipe (|k| <= 8 modes) on a 16 x 32 x 64 grid: the modes sit at the x Nyquist
-    limit.  lam^S = m1 - m^S cancels (kappa = ||m^S|| / ||m1 - m^S||), so the fp32 forward error
-    (~ 7e-8 per step, measured) is amplified by kappa in lam and by the derivative in b.  The
-    tolerance is derived from that arithmetic: TOL_lam = 1e-5 + 4 eps_32 n_t kappa."""
+    limit, and lam^S = m1 - m^S cancels strongly.  Same rule as test_eval_gradient (DESIGN.md
+    §8.1): the forward sweep at TOL, lam and b at TOL plus the forward error propagated by the
+    oracle's own adjoint / body force from the GPU's lam^S."""
     d = case(5, (16, 32, 64), model=1)
     t = topt_for(d)
     t.eval_gradient(dev(d["m0"]), dev(d["m1"]), dev(d["v"]))
     ref = ogr.evaluate(d["prob"], d["v"])
     lam, b = t.adjoint()
-    kappa = np.linalg.norm(ref["m"][-1]) / np.linalg.norm(ref["lam"][-1])
-    tol = 1e-5 + 4 * 6e-8 * d["nt"] * kappa
-    assert rel_l2(host(lam)[-1], ref["lam"][-1]) < tol
-    assert rel_l2(host(b), ref["b"]) < 4 * tol
+    lam, b = host(lam), host(b)
+    m = host(t.forward(dev(d["m0"]), dev(d["v"])))
+    assert rel_l2(m[-1], ref["m"][-1]) < TOL
+    plam, pb, _ = _propagated(d, ref, lam[-1])
+    for j in (0, d["nt"]):
+        assert rel_l2(lam[j], ref["lam"][j]) < TOL + rel_l2(plam[j], ref["lam"][j]), j
+    assert rel_l2(b, ref["b"]) < TOL + rel_l2(pb, ref["b"])
 
 
 def test_forward_large_displacement_fallback():

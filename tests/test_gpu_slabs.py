@@ -33,8 +33,7 @@ def test_eval_gradient_slab_invariance(model, P, transport):
     for k in ("obj", "dist", "reg", "grad_inf", "gs", "slv", "sls"):
         assert abs(a[k] - b[k]) <= 1e-6 * abs(a[k]) + 1e-30, k
     ref = ogr.evaluate(d["prob"], d["v"])
-    kappa = max(1.0, np.linalg.norm(ref["m"][-1]) / np.linalg.norm(ref["lam"][-1]))
-    assert rel_l2(gp, ref["g"]) < 1e-5 * kappa
+    assert rel_l2(gp, ref["g"]) < 1e-5
     assert rel_l2(sp, ref["s"]) < 1e-5
 
 
@@ -90,10 +89,42 @@ def test_transport_and_peer_arguments_checked():
     assert LIB.topt_set_peer_workspaces(t.ctx, bases, 0) == 0   # clear
 
 
-def test_halo_overflow_is_reported():
-    """A foot more than 3 cells away in z cannot be served by the neighbour's halo planes."""
-    import paper_2510_08782_b200 as topt
-    d = case(2, (64, 32, 32), scale=6.0)
-    t = topt_for(d, world=4, max_iter=2, eps_rel=0.0)
-    with pytest.raises(topt.ToptError, match="HALO"):
-        t.solve(dev(d["m0"]), dev(d["m1"]), dev(d["v"]))
+@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("scale", [4.0, 24.0])
+def test_large_feet_window_matches_single_slab(P, scale):
+    """Feet far beyond the stored 4-plane halo (|delta_z| ~ 5 and ~ 28 cells on a 32-plane grid:
+    the window is sized from max |delta_z|, gathered over several slabs when it is wider than
+    one (P = 8: 4 planes per slab), and wraps a whole period at the larger scale; SL has no CFL
+    limit): the P-slab evaluation equals the single-slab one."""
+    d = case(2, (64, 32, 32), model=1, scale=scale)
+    t1 = topt_for(d)
+    df, _ = t1.feet(dev(d["v"]))
+    dz = float(np.max(np.abs(host(df)[2])))
+    assert dz > 3.0 and (scale < 10 or dz > 16.0), dz
+    g1, s1, sc1 = t1.eval_gradient(dev(d["m0"]), dev(d["m1"]), dev(d["v"]))
+    tp = topt_for(d, world=P)
+    gp, sp, scp = tp.eval_gradient(dev(d["m0"]), dev(d["m1"]), dev(d["v"]))
+    assert rel_l2(host(gp), host(g1)) < 1e-6
+    assert rel_l2(host(sp), host(s1)) < 1e-6
+    a, b = t1.scalars_dict(sc1), tp.scalars_dict(scp)
+    for k in ("obj", "dist", "grad_inf", "gs"):
+        assert abs(a[k] - b[k]) <= 1e-6 * abs(a[k]), k
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_solve_with_trial_feet_beyond_halo(P):
+    """GA-NGMRES from v^0 = 4 v*: the Armijo trials' feet reach |delta_z| > 3 cells.  No trial is
+    rejected for halo reasons (the window is sized per evaluation), so the P-slab solve takes the
+    single-slab step sequence."""
+    d = case(2, (64, 32, 32), scale=4.0)
+    t1 = topt_for(d)
+    df, _ = t1.feet(dev(d["v"]))
+    assert float(np.max(np.abs(host(df)[2]))) > 3.0
+    t1 = topt_for(d, max_iter=8, eps_rel=0.0)
+    v1, r1 = t1.solve(dev(d["m0"]), dev(d["m1"]), dev(d["v"]))
+    tp = topt_for(d, world=P, max_iter=8, eps_rel=0.0)
+    vp, rp = tp.solve(dev(d["m0"]), dev(d["m1"]), dev(d["v"]))
+    assert rp["iters"] == r1["iters"] == 8
+    assert (rp["obj_evals"], rp["grad_evals"], rp["rho"]) == (r1["obj_evals"], r1["grad_evals"], r1["rho"])
+    assert abs(rp["obj"] - r1["obj"]) <= 1e-6 * abs(r1["obj"])
+    assert rel_l2(host(vp), host(v1)) < 1e-5
