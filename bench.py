@@ -469,7 +469,6 @@ def run_topt(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        del d
         sec, stages = oracle_stage_sample(tuple(cfgp["n"]), str(dev))
         cpu = {"value": 1.0 / sec, "unit": UNIT, "cores": _cpu_threads(), "kind": "oracle",
                "sample": f"fp64 oracle (oracle/, numba + numpy, as it stands) on the {'x'.join(map(str, cfgp['n']))} "

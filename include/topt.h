@@ -270,6 +270,16 @@ topt_status topt_multidot(topt_ctx* ctx, const float* a, const float* const* bs,
 topt_status topt_mix(topt_ctx* ctx, const float* q, const float* const* vs, const double* beta,
                      int32_t count, float* out, void* stream);
 
+/* NGMRES(w) (Alg. 1) on the LINEAR fixed-point map q(v) = v - omega g(v),
+ * g(v) = A v - b, A = I + alpha L (L of the context's reg_order, alpha L applied by the fp64
+ * spectral chain, R4): the solver's Gram multi-dot, host fp64 LSQ and mixing kernels on a problem
+ * whose NGMRES(infinity) iterates equal GMRES's.  b: d*F device input; v_inout: d*F
+ * device, the start iterate in, v^{iters} out; res: HOST double[iters + 1], res[k] = ||g(v^k)||_2
+ * (unweighted).  Single slab, advection or continuity context (TOPT_ERR_UNSUPPORTED otherwise).
+ * Synchronous; uses the workspace. */
+topt_status topt_linear_ngmres(topt_ctx* ctx, const float* b, double omega, float* v_inout, int32_t iters,
+                               double* res, void* stream);
+
 /* ---- instrumentation -------------------------------------------------------------------- */
 
 /* enable != 0: bracket every launch group of the hot path with CUDA events on the caller's

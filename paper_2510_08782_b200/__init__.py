@@ -282,6 +282,18 @@ class Topt:
         check(LIB.topt_mix(self.ctx, _ptr(q), arr, b, len(vs), _ptr(out), _stream()), "topt_mix")
         return out
 
+    def linear_ngmres(self, b, omega, iters, v0=None):
+        """NGMRES(window) on q(v) = v - omega (A v - b), A = I + alpha L (topt_linear_ngmres).
+        Returns (v, [||A v^k - b||_2 for k = 0..iters])."""
+        vshape = (self.d,) + self.shape
+        b = _f32(b, self.device, vshape)
+        v = torch.zeros(vshape, dtype=torch.float32, device=self.device) if v0 is None \
+            else _f32(v0, self.device, vshape).clone()
+        res = (ctypes.c_double * (iters + 1))()
+        check(LIB.topt_linear_ngmres(self.ctx, _ptr(b), float(omega), _ptr(v), int(iters), res, _stream()),
+              "topt_linear_ngmres")
+        return v, list(res)
+
     # -- instrumentation
     def profile(self, enable: bool = True):
         check(LIB.topt_profile(self.ctx, 1 if enable else 0), "topt_profile")

@@ -67,6 +67,7 @@ SIGNATURES = {
     "topt_local_slab": (_I, [_P, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     "topt_set_transport": (_I, [_P, _I]),
     "topt_get_transport": (_I, [_P]),
+    "topt_linear_ngmres": (_I, [_P, _P, ctypes.c_double, _P, _I, ctypes.POINTER(ctypes.c_double), _P]),
     "topt_set_peer_workspaces": (_I, [_P, ctypes.POINTER(_P), _I]),
     "topt_solve": (_I, [_P, _P, _P, _P, ctypes.POINTER(Report), _P]),
     "topt_set_step_replay": (_I, [_P, ctypes.POINTER(ctypes.c_double), _I]),

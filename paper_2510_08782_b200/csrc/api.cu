@@ -1499,6 +1499,92 @@ topt_status topt_mix(topt_ctx* c, const float* q, const float* const* vs, const 
   return TOPT_OK;
 }
 
+// NGMRES(w) (Alg. 1) on the linear fixed-point map q(v) = v - omega g(v), g(v) = A v - b,
+// A = I + alpha L (the v-chain, fp64) — the same Gram multi-dot, host LSQ and mixing kernels as
+// topt_solve, on a problem whose NGMRES(infinity) iterates are GMRES's.
+topt_status topt_linear_ngmres(topt_ctx* c, const float* b, double omega, float* v_inout, int32_t iters,
+                               double* res, void* stream) {
+  topt_status s0 = need_ws(c);
+  if (s0 != TOPT_OK) return s0;
+  if (c->comm.P > 1) return fail(TOPT_ERR_UNSUPPORTED, "linear NGMRES runs on one slab");
+  if (c->p.model == TOPT_INCOMPRESSIBLE) return fail(TOPT_ERR_UNSUPPORTED, "A = I + alpha L needs a non-Leray model");
+  if (!b || !v_inout || iters < 0 || !res) return fail(TOPT_ERR_INVALID_ARG, "bad argument");
+  if (!aligned16(b) || !aligned16(v_inout)) return fail(TOPT_ERR_INVALID_ARG, "pointers must be 16-byte aligned");
+  cudaStream_t st = (cudaStream_t)stream;
+  Slab& sl = c->slabs[0];
+  const size_t V = c->vecN;
+  const int W1 = c->p.window + 1;
+  // g(x) = x + alpha L x - b into out
+  auto apply_g = [&](const float* x, float* out) {
+    std::vector<Io> io(1);
+    io[0] = Io{nullptr, nullptr, x, nullptr, nullptr, nullptr, sl.pub(4), sl.intl(4)};
+    run_vchain(c, io, st);
+    launch_axpy(x, 1.0f, sl.utmp, V, out, st);
+    launch_axpy(out, -1.0f, b, V, out, st);
+  };
+  auto norm2 = [&](const float* x, double& out) -> topt_status {
+    std::vector<double> dd;
+    topt_status rr = host_dots(c, [x](Slab&) { return x; }, {[x](Slab&) { return x; }}, dd, st);
+    out = rr == TOPT_OK ? std::sqrt(dd[0]) : 0.0;
+    return rr;
+  };
+  auto slotA = [&](int i) { return sl.hist + (size_t)(3 * i) * V; };
+  auto slotB = [&](int i) { return sl.hist + (size_t)(3 * i + 1) * V; };
+  std::deque<int> win;
+  std::vector<std::vector<double>> H(W1, std::vector<double>(W1, 0.0));
+  auto push = [&](const float* v, const float* g) -> topt_status {
+    int slot;
+    if ((int)win.size() < W1) slot = (int)win.size();
+    else { slot = win.front(); win.pop_front(); }
+    cudaMemcpyAsync(slotA(slot), v, V * 4, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(slotB(slot), g, V * 4, cudaMemcpyDeviceToDevice, st);
+    win.push_back(slot);
+    std::vector<std::function<const float*(Slab&)>> bs;
+    for (int s2 : win) bs.push_back([&, s2](Slab&) { return (const float*)slotB(s2); });
+    std::vector<double> dd;
+    topt_status rr = host_dots(c, [&, slot](Slab&) { return (const float*)slotB(slot); }, bs, dd, st);
+    for (size_t i = 0; i < win.size() && rr == TOPT_OK; ++i) H[slot][win[i]] = H[win[i]][slot] = dd[i];
+    return rr;
+  };
+  TOPT_CUDA(cudaMemcpyAsync(sl.vcur, v_inout, V * 4, cudaMemcpyDeviceToDevice, st));
+  apply_g(sl.vcur, sl.gcur);
+  topt_status r;
+  if ((r = norm2(sl.gcur, res[0])) != TOPT_OK) return r;
+  if ((r = push(sl.vcur, sl.gcur)) != TOPT_OK) return r;
+  for (int k = 0; k < iters; ++k) {
+    launch_axpy(sl.vcur, (float)(-omega), sl.gcur, V, sl.q, st);  // q = v - omega g
+    apply_g(sl.q, sl.gq);
+    const int m = (int)win.size();
+    std::vector<std::function<const float*(Slab&)>> bs;
+    for (int i = 0; i < m; ++i) { const int si = win[m - 1 - i]; bs.push_back([&, si](Slab&) { return (const float*)slotB(si); }); }
+    bs.push_back([&](Slab&) { return (const float*)sl.gq; });
+    std::vector<double> rd;
+    if ((r = host_dots(c, [&](Slab&) { return (const float*)sl.gq; }, bs, rd, st)) != TOPT_OK) return r;
+    const double gam = rd[m];
+    std::vector<double> G(m * m), rhs(m);
+    for (int i = 0; i < m; ++i) {
+      rhs[i] = gam - rd[i];
+      for (int j = 0; j < m; ++j) G[i * m + j] = gam - rd[i] - rd[j] + H[win[m - 1 - i]][win[m - 1 - j]];
+    }
+    std::vector<double> beta = lsq_from_gram(m, G, rhs);
+    std::vector<const float*> vs;
+    for (int i = 0; i < m; ++i) vs.push_back(slotA(win[m - 1 - i]));
+    {
+      Prof pr(c, K_MIX, (vs.size() + 2.0) * V * 4.0, 1, st);
+      launch_mix(sl.q, vs.data(), beta.data(), m, V, sl.vnew, st);
+    }
+    apply_g(sl.vnew, sl.gnew);
+    std::swap(sl.vcur, sl.vnew);
+    std::swap(sl.gcur, sl.gnew);
+    if ((r = norm2(sl.gcur, res[k + 1])) != TOPT_OK) return r;
+    if ((r = push(sl.vcur, sl.gcur)) != TOPT_OK) return r;
+  }
+  TOPT_CUDA(cudaMemcpyAsync(v_inout, sl.vcur, V * 4, cudaMemcpyDeviceToDevice, st));
+  TOPT_CUDA(cudaStreamSynchronize(st));
+  TOPT_CHECK_LAUNCH();
+  return TOPT_OK;
+}
+
 topt_status topt_profile(topt_ctx* c, int32_t enable) {
   if (!c) return fail(TOPT_ERR_INVALID_ARG, "ctx is NULL");
   TOPT_CUDA(cudaDeviceSynchronize());
@@ -1793,25 +1879,45 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
       (void)wk;
       if ((r = push(Vc, Gc, Uc, true)) != TOPT_OK) return r;
     } else {
-      // AA (Alg. 2): r_k = v^k - q(v^k); LSQ over r_k - r_{k-i}, i = 1..w_k; mix q-images
+      // AA (Alg. 2): r_k = v^k - q(v^k); LSQ over r_k - r_{k-i}, i = 1..w_k; mix q-images.
+      // ONE multi-dot pass per step: <r_k, r_i> for every window slot and <r_k, r_k>; the
+      // <r_i, r_j> come from the cached Gram H (rows filled when each r_i was pushed), exactly
+      // the values a recomputation would give (fp64 sums of exact fp32 products, fixed order).
       for (auto& sl : c->slabs) launch_sub(sl.vcur, sl.q, V, sl.vt, st);  // r_k
       const int m = std::min((int)win.size(), wk);
-      if (!fp_step && m > 0) {
+      const int nw = (int)win.size();
+      std::vector<double> rd;  // rd[i] = <r_k, r_{slot win[nw-1-i]}>, rd[nw] = <r_k, r_k>
+      {
         const double tl = now();
         std::vector<CAcc> bs;
-        for (int i = 0; i < m; ++i) bs.push_back(cacc(slotA(win[win.size() - 1 - i])));
+        for (int i = 0; i < nw; ++i) bs.push_back(cacc(slotA(win[nw - 1 - i])));
         bs.push_back(cacc(Vt));
-        std::vector<double> rd;
         if ((r = host_dots(c, cacc(Vt), bs, rd, st)) != TOPT_OK) return r;
-        const double gam = rd[m];
+        t_ls += now() - tl;
+      }
+      const double gam = rd[nw];
+      // push r_k (slot A), q (slot B), u(q) with its Gram row from rd
+      auto push_r = [&]() {
+        std::vector<int> old(win.begin(), win.end());
+        const int slot = take_slot();
+        copyv(slotA(slot), Vt);
+        copyv(slotB(slot), Q);
+        copyv(slotU(slot), Uq);
+        for (int i = 0; i < nw; ++i) {
+          const int so = old[nw - 1 - i];
+          if (so == slot) continue;  // evicted
+          H[slot][so] = H[so][slot] = rd[i];
+        }
+        H[slot][slot] = gam;
+        win.push_back(slot);
+      };
+      if (!fp_step && m > 0) {
+        const double tl = now();
         std::vector<double> G(m * m), rhs(m);
         for (int i = 0; i < m; ++i) {
-          std::vector<CAcc> b2;
-          for (int j = 0; j < m; ++j) b2.push_back(cacc(slotA(win[win.size() - 1 - j])));
-          std::vector<double> row;
-          if ((r = host_dots(c, cacc(slotA(win[win.size() - 1 - i])), b2, row, st)) != TOPT_OK) return r;
+          const int si = win[nw - 1 - i];
           rhs[i] = gam - rd[i];
-          for (int j = 0; j < m; ++j) G[i * m + j] = gam - rd[i] - rd[j] + row[j];
+          for (int j = 0; j < m; ++j) G[i * m + j] = gam - rd[i] - rd[j] + H[si][win[nw - 1 - j]];
         }
         std::vector<double> xi = lsq_from_gram(m, G, rhs);
         t_ls += now() - tl;
@@ -1822,14 +1928,14 @@ topt_status topt_solve(topt_ctx* c, const float* m0, const float* m1, float* v_i
         }
         mix_into(Vn, Q, qv, xi);
         mix_into(Un, Uq, qu, xi);
-        if ((r = push(Vt, Q, Uq, false)) != TOPT_OK) return r;
+        push_r();
         te = now();
         if ((r = eval_new()) != TOPT_OK) return r;
         t_pde += now() - te;
         t_f += now() - te;
         ++nsteps;
       } else {
-        if ((r = push(Vt, Q, Uq, false)) != TOPT_OK) return r;
+        push_r();
         te = now();
         if ((r = eval_into(Q, Uq, Gq, Sq, 2, qs)) != TOPT_OK) return r;
         t_pde += now() - te;

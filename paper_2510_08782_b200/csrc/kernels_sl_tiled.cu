@@ -26,6 +26,7 @@
 #include <cmath>
 
 #include "internal.cuh"
+#include "tma.cuh"
 
 namespace topt {
 
@@ -174,7 +175,11 @@ constexpr int NZR = 16;                         // ring slots (power of two)
 static_assert(NZR >= 2 * H + (D + 1) * K, "ring too small");
 constexpr int PS = tiled::Cfg<H>::PS, PH = tiled::Cfg<H>::PH;
 constexpr int NF4 = PH * (tiled::XW / 4);  // float4 per plane
-constexpr size_t SMEM = (size_t)NZR * PS * sizeof(float);
+#ifndef TOPT_SL_TMA
+#define TOPT_SL_TMA 0  // 1: ring filled by TMA bulk row copies on mbarriers (measured slower)
+#endif
+constexpr int NGRP = NZR / K;  // TMA: plane groups of K slots, one mbarrier each
+constexpr size_t SMEM = (size_t)NZR * PS * sizeof(float) + (TOPT_SL_TMA ? NGRP * sizeof(uint64_t) : 0);
 }  // namespace pipe
 
 #ifndef TOPT_TRACE2
@@ -240,12 +245,55 @@ __global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, T
   };
 
   const int nst = ZC / K;
+#if TOPT_SL_TMA
+  // TMA ring fill: the K planes of a group (K x PH rows of XW floats, periodic in x and y) are
+  // copied by warp 0 with bulk copies completing on the group's mbarrier; stage s reads groups
+  // s-1, s, s+1 (H == K) and, after its barrier, warp 0 refills the group stage s-1 released with
+  // group s+2.  Every thread tracks the groups' phase parities in `phase`.
+  static_assert(H == K && pipe::D == 1, "TMA ring: halo of one group, prefetch distance one stage");
+  (void)load_planes;
+  (void)load_stage;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + NZR * PS);
+  auto tma_group = [&](int pa) {  // warp 0: planes [pa, pa + K)
+    uint64_t* bar = bars + ((pa & (NZR - 1)) / K);
+    if (threadIdx.x == 0) tma::mbar_arrive_expect_tx(bar, K * pipe::PH * XW * 4);
+    __syncwarp();
+    for (int q = threadIdx.x; q < K * pipe::PH; q += 32) {
+      const int pl = pa + q / pipe::PH, r = q % pipe::PH;
+      float* dst = sm + (pl & (NZR - 1)) * PS + r * PW;
+      const float* row = in + psrc(pl) + (size_t)((y0 - H + r) & (g.ny - 1)) * g.nx;
+      for (int c = 0; c < XW;) {  // columns x0 - XH .. x0 + TX + XH - 1: up to 3 contiguous runs
+        const int gx = (x0 - XH + c) & (g.nx - 1);
+        const int len = min(XW - c, g.nx - gx);
+        tma::bulk_g2s(dst + c, row + gx, (unsigned)len * 4u, bar);
+        c += len;
+      }
+    }
+  };
+  unsigned phase = 0;
+  auto wait_group = [&](int pa) {
+    const int gi = (pa & (NZR - 1)) / K;
+    tma::mbar_wait(bars + gi, (phase >> gi) & 1u);
+    phase ^= 1u << gi;
+  };
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < pipe::NGRP; ++i) tma::mbar_init(bars + i, 1);
+    tma::fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tma_group(z0 - H);
+    tma_group(z0);
+    tma_group(z0 + K);
+  }
+#else
   load_planes(z0 - H, z0 + K + H);  // stage 0
   cp_commit();
   for (int u = 1; u < pipe::D; ++u) {  // stages 1 .. D-1
     if (u < nst) load_stage(z0 + u * K + H);
     cp_commit();
   }
+#endif
 
   const size_t gi0 = (size_t)z0 * plane + (size_t)(y0 + ty) * g.nx + x0 + tx;
   // per-thread stream bases; offsets from them fit 32 bits (3F < 2^32 for every supported grid)
@@ -269,10 +317,20 @@ __global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, T
   for (int st = 0; st < nst; ++st) {
     // one barrier per stage: after it every thread has finished stage st-1, whose oldest
     // K slots (planes needed by no later stage, NZR >= 2H + (D+1)K) take stage st+D's planes
+#if TOPT_SL_TMA
+    if (st == 0) {
+      wait_group(z0 - H);
+      wait_group(z0);
+    }
+    wait_group(z0 + (st + 1) * K);
+    __syncthreads();
+    if (threadIdx.x < 32 && st + 1 < nst) tma_group(z0 + (st + 2) * K);
+#else
     cp_wait<pipe::D - 1>();
     __syncthreads();
     if (st + pipe::D < nst) load_stage(z0 + (st + pipe::D) * K + H);
     cp_commit();
+#endif
 #pragma unroll 1
     for (int j = 0; j < K; ++j) {
       const int zi = st * K + j, z = z0 + zi;
@@ -352,7 +410,9 @@ __global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, T
       }
     }
   }
+#if !TOPT_SL_TMA
   cp_wait<0>();
+#endif
 
   if (MODE == M_LAST) {
     __shared__ double red[8];

@@ -31,6 +31,9 @@
 
 #include "internal.cuh"
 #include "rfft.cuh"
+#include "tma.cuh"
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 namespace topt {
 
@@ -452,6 +455,163 @@ static void rds_pf_launch(const Geom& g, int axis, const DerivArgs& a, const Der
                                                  a.beta, a.out, (int)items);
 }
 
+// =====================================================================================
+// Body-force accumulation along a strided axis with TMA staging (k_rds_tma).  Same arithmetic
+// and thread layout as k_rds (thread (c, t), c fastest; TXC = kThreads / T columns of complex
+// pairs), but the slice tiles psi_j and lam_j — N positions x 2 TXC floats — are brought in by
+// TMA TENSOR copies (one per 256 positions and field, issued by one thread, completing on the
+// slot's mbarrier) ONE SLICE AHEAD into a two-slot ring, so the next slice streams in while the
+// current one is transformed, with no registers spent on the prefetch.  The tensor maps view
+// the S+1 slices as a 4D tensor (x, y, z, slice).  The psi tile doubles as the FFT exchange
+// scratch once its values are in registers (interleaved [position][column] layout,
+// conflict-free: a warp's 16 columns x 2 positions are 32 consecutive complex words).  The
+// (item, slice) sequence of a persistent block is pipelined across items.
+// =====================================================================================
+struct TmaDeriv {
+  CUtensorMap psi, lam;  // 4D (x, y, z, slice), box (2 TXC, N or 1, 1 or N, 1) capped at 256 positions
+};
+template <int N>
+__global__ void __launch_bounds__(kThreads, 1) k_rds_tma(Geom g, int axis, const __grid_constant__ TmaDeriv tm,
+                                                         bool has_lam, DerivWeights w, int J, float beta,
+                                                         float* __restrict__ out, int nitems) {
+  constexpr int E = Ev<N, 16>::v, T = N / E, TXC = kThreads / T;
+  constexpr int TILE = N * 2 * TXC;  // floats per staged tile
+  constexpr int BOX = N < 256 ? N : 256;
+  extern __shared__ __align__(128) float smf[];
+  float* tiles = smf;                                            // [slot][psi, lam][N][2 TXC]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smf + 4 * TILE);  // one per slot
+  const int c = threadIdx.x % TXC, t = threadIdx.x / TXC;
+  float2 tw[RfCfg<N, E>::NTW];
+  rf_twiddles<N, E>(tw, t);
+  const int tilesx = g.nx / (2 * TXC);
+  const size_t S = axis == 1 ? (size_t)g.nx : (size_t)g.nx * g.ny;
+  const float invN = 1.0f / (float)N;
+  const int nmine = blockIdx.x < nitems ? (nitems - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int total = nmine * J;
+  // thread 0: stage slice k of this block's sequence (item blockIdx.x + (k / J) gridDim.x, slice k % J)
+  auto issue = [&](int k) {
+    const int slot = k & 1, item = blockIdx.x + (k / J) * gridDim.x, j = k % J;
+    const int x0 = (item % tilesx) * 2 * TXC, outer = item / tilesx;
+    float* dp = tiles + (2 * slot) * TILE;
+    tma::mbar_arrive_expect_tx(bars + slot, (has_lam ? 2u : 1u) * TILE * 4u);
+    for (int p0 = 0; p0 < N; p0 += BOX) {
+      const int cy = axis == 1 ? p0 : outer, cz = axis == 1 ? outer : p0;
+      tma::tensor4_g2s(dp + p0 * 2 * TXC, &tm.psi, x0, cy, cz, j, bars + slot);
+      if (has_lam) tma::tensor4_g2s(dp + TILE + p0 * 2 * TXC, &tm.lam, x0, cy, cz, j, bars + slot);
+    }
+  };
+  if (threadIdx.x == 0) {
+    tma::mbar_init(bars, 1);
+    tma::mbar_init(bars + 1, 1);
+    tma::fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && total > 0) issue(0);
+  float2 acc[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) acc[e] = make_float2(0.f, 0.f);
+  for (int k = 0; k < total; ++k) {
+    const int slot = k & 1, j = k % J;
+    // slot (k+1)&1 held slice k-1: every thread left it at the end-of-slice barrier below
+    if (threadIdx.x == 0 && k + 1 < total) issue(k + 1);
+    tma::mbar_wait(bars + slot, (unsigned)(k >> 1) & 1u);
+    float2* tp = reinterpret_cast<float2*>(tiles + (2 * slot) * TILE);
+    const float2* tl = reinterpret_cast<const float2*>(tiles + (2 * slot + 1) * TILE);
+    float2 z[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) z[e] = tp[(t + T * e) * TXC + c];
+    __syncthreads();  // the psi tile becomes the exchange scratch
+    rf_fft<N, E, false, false, false, TXC>(z, tp + c, t, tw);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const float kk = kprime(t + T * e, N) * invN;
+      z[e] = make_float2(-kk * z[e].y, kk * z[e].x);
+    }
+    rf_fft<N, E, true, false, false, TXC>(z, tp + c, t, tw);
+    const float wj = w.w[j];
+    if (has_lam) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const float2 l = tl[(t + T * e) * TXC + c];
+        acc[e].x = fmaf(wj * l.x, z[e].x, acc[e].x);
+        acc[e].y = fmaf(wj * l.y, z[e].y, acc[e].y);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        acc[e].x = fmaf(wj, z[e].x, acc[e].x);
+        acc[e].y = fmaf(wj, z[e].y, acc[e].y);
+      }
+    }
+    if (j == J - 1) {
+      const int item = blockIdx.x + (k / J) * gridDim.x;
+      const int x0 = (item % tilesx) * 2 * TXC, outer = item / tilesx;
+      const size_t b0 = (axis == 1 ? ((size_t)outer << (g.lx + g.ly)) : ((size_t)outer << g.lx)) + x0 + 2 * c;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        float2* o = reinterpret_cast<float2*>(out + b0 + (t + T * e) * S);
+        float2 r = acc[e];
+        if (beta != 0.0f) {
+          const float2 p = *o;
+          r.x += beta * p.x;
+          r.y += beta * p.y;
+        }
+        *o = r;
+        acc[e] = make_float2(0.f, 0.f);
+      }
+    }
+    __syncthreads();  // slot k&1 (tiles and scratch) free for slice k+2
+  }
+}
+
+#ifndef TOPT_RDS_TMA
+#define TOPT_RDS_TMA 1
+#endif
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+// 4D map of the slices of a field: dims (nx, ny, nz, J), slice stride `stride` floats
+static bool slice_map(CUtensorMap* m, const float* base, const Geom& g, size_t stride, int J, int axis, int box_x,
+                      int box_n) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[4] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.nz, (cuuint64_t)J};
+  const cuuint64_t strides[3] = {(cuuint64_t)g.nx * 4, (cuuint64_t)g.nx * g.ny * 4, (cuuint64_t)stride * 4};
+  const cuuint32_t box[4] = {(cuuint32_t)box_x, (cuuint32_t)(axis == 1 ? box_n : 1), (cuuint32_t)(axis == 1 ? 1 : box_n),
+                             1u};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+template <int N>
+static bool rds_tma_launch(const Geom& g, int axis, const DerivArgs& a, const DerivWeights& w, cudaStream_t st) {
+  constexpr int T = N / Ev<N, 16>::v, TXC = kThreads / T;
+  if (!TOPT_RDS_TMA || N < 128 || N > 1024 || 2 * TXC > g.nx || g.nx % (2 * TXC)) return false;
+  if (((uintptr_t)a.psi | (uintptr_t)(a.lam ? a.lam : a.psi)) & 15) return false;
+  if ((a.psi_stride | (a.lam ? a.lam_stride : 0)) & 3) return false;
+  TmaDeriv tm{};
+  const int box_n = N < 256 ? N : 256;
+  if (!slice_map(&tm.psi, a.psi, g, a.psi_stride, a.J, axis, 2 * TXC, box_n)) return false;
+  if (a.lam && !slice_map(&tm.lam, a.lam, g, a.lam_stride, a.J, axis, 2 * TXC, box_n)) return false;
+  const size_t sm = 4 * (size_t)N * 2 * TXC * sizeof(float) + 2 * sizeof(uint64_t);
+  const int outer = axis == 1 ? g.nz : g.ny;
+  const long long items = (long long)(g.nx / (2 * TXC)) * outer;
+  const int blocks = persistent_blocks(k_rds_tma<N>, kThreads, sm, items);
+  k_rds_tma<N><<<blocks, kThreads, sm, st>>>(g, axis, tm, a.lam != nullptr, w, a.J, a.beta, a.out, (int)items);
+  return true;
+}
+
 template <int N, int EMAX>
 static void rds_launch(const Geom& g, int axis, const DerivArgs& a, const DerivWeights& w, cudaStream_t st) {
   constexpr int E = Ev<N, EMAX>::v, T = N / E;
@@ -485,8 +645,12 @@ static void deriv_dispatch(const Geom& g, int axis, const DerivArgs& a, const De
     // time-slice sums: one smem exchange per FFT; at N >= 512 (one resident block per SM)
     // the tiles of the next slice are prefetched with cp.async (measured: +7% at 512^3,
     // -10% at 256^3 where two blocks per SM already overlap the loads)
-    if constexpr (N >= 512) rds_pf_launch<N, 16>(g, axis, a, w, st);
-    else rds_launch<N, 16>(g, axis, a, w, st);
+    if (rds_tma_launch<N>(g, axis, a, w, st)) {
+    } else if constexpr (N >= 512) {
+      rds_pf_launch<N, 16>(g, axis, a, w, st);
+    } else {
+      rds_launch<N, 16>(g, axis, a, w, st);
+    }
   }
   count_launch();
 }

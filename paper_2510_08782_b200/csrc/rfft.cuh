@@ -97,7 +97,13 @@ __device__ __forceinline__ void rf_sync() {
   else __syncthreads();
 }
 
-template <int N, int E, int NS, int OFF, bool INV, bool WARP, bool FULL, typename C>
+// scratch addressing of the stage-boundary exchange: LS == 0 -> line[fft_pad(i)] (a padded line of
+// its own); LS > 0 -> line[i * LS] (lines interleaved with stride LS: a [position][line] tile, e.g. a
+// TMA-staged input tile reused as scratch once its values are in registers)
+template <int LS>
+__device__ __forceinline__ int rf_idx(int i) { return LS == 0 ? fft_pad(i) : i * LS; }
+
+template <int N, int E, int NS, int OFF, bool INV, bool WARP, bool FULL, int LS, typename C>
 __device__ __forceinline__ void rf_stage(C (&a)[E], C* line, int t, const C* tw) {
   constexpr int R = rf_rad(N, E, NS), B = E / R, T = N / E, NB = rf_nb(R, FULL);
   constexpr bool LAST = NS * R == N;
@@ -131,22 +137,22 @@ __device__ __forceinline__ void rf_stage(C (&a)[E], C* line, int t, const C* tw)
       const int j = t + b * T;
       const int base = (j / NS) * NS * R + (j & (NS - 1));
 #pragma unroll
-      for (int q = 0; q < R; ++q) line[fft_pad(base + q * NS)] = o[b + q * B];
+      for (int q = 0; q < R; ++q) line[rf_idx<LS>(base + q * NS)] = o[b + q * B];
     }
     rf_sync<WARP>();
 #pragma unroll
-    for (int e = 0; e < E; ++e) a[e] = line[fft_pad(t + T * e)];
+    for (int e = 0; e < E; ++e) a[e] = line[rf_idx<LS>(t + T * e)];
     rf_sync<WARP>();
-    rf_stage<N, E, NS * R, OFF + (NS > 1 ? B * NB : 0), INV, WARP, FULL, C>(a, line, t, tw);
+    rf_stage<N, E, NS * R, OFF + (NS > 1 ? B * NB : 0), INV, WARP, FULL, LS, C>(a, line, t, tw);
   }
 }
 
 // Unnormalised DFT of the line held in a[] (forward exp(-i k x), inverse exp(+i k x)).
 // `line` is this line's smem scratch (RfCfg::STRIDE complex); `tw` from rf_twiddles with the
 // same FULL; every thread of the sync group (warp if WARP, else block) must call it.
-template <int N, int E, bool INV, bool WARP, bool FULL = false, typename C>
+template <int N, int E, bool INV, bool WARP, bool FULL = false, int LS = 0, typename C>
 __device__ __forceinline__ void rf_fft(C (&a)[E], C* line, int t, const C* tw) {
-  rf_stage<N, E, 1, 0, INV, WARP, FULL, C>(a, line, t, tw);
+  rf_stage<N, E, 1, 0, INV, WARP, FULL, LS, C>(a, line, t, tw);
 }
 
 }  // namespace topt

@@ -3,8 +3,10 @@
 The paper's experiments are grids of solver settings on one registration problem:
   * wst   — w in {1, 5, 10, 15, 20, 25, 50} x (sigma, tau) in {(1,0), (5,1), (1,5), (5,5)}
             (P:294; tables T2/T3);
-  * alpha — alpha in {1e-1, 1e-2, 1e-3, 1e-4} at fixed (w; sigma, tau) (P:505);
-  * mesh  — n in {64, 128, 256, 512} with n_t = 4, 8, 16, 32 (P:680).
+  * alpha — alpha in {1e-1, 5e-2, 1e-2, 5e-3, 1e-3, 5e-4} x (sigma, tau) in {(5,1), (4,2)} x
+            w in {10, 15, 20, 25} (P:505);
+  * mesh  — n in {64, 128, 256, 512} with n_t = 4, 8, 16, 32, alpha = 1e-3, w = 25,
+            (sigma, tau) = (4, 2), eps_rel = 1e-3 (caption of the mesh table).
 Every cell is an independent solve from v^0 = 0 (one replica per GPU: cells are dealt
 round-robin to the ranks of `torchrun --nproc-per-node N sweep.py ...`, no collective on the
 data path).  The problem is the config-1 recipe (BASELINE.json: 4 seeded Gaussians
@@ -27,6 +29,9 @@ sys.path.insert(0, ROOT)
 
 WST_W = [1, 5, 10, 15, 20, 25, 50]
 WST_P = [(1, 0), (5, 1), (1, 5), (5, 5)]
+ALPHA_A = [1e-1, 5e-2, 1e-2, 5e-3, 1e-3, 5e-4]
+ALPHA_P = [(5, 1), (4, 2)]
+ALPHA_W = [10, 15, 20, 25]
 
 
 def cells_for(grid: str, n: int, nt: int, alpha: float, w: int, sigma: int, tau: int):
@@ -34,9 +39,10 @@ def cells_for(grid: str, n: int, nt: int, alpha: float, w: int, sigma: int, tau:
     if grid == "wst":
         return [dict(n=n, nt=nt, alpha=alpha, window=ww, sigma=s, tau=t) for (s, t) in WST_P for ww in WST_W]
     if grid == "alpha":
-        return [dict(n=n, nt=nt, alpha=a, window=w, sigma=sigma, tau=tau) for a in (1e-1, 1e-2, 1e-3, 1e-4)]
+        return [dict(n=n, nt=nt, alpha=a, window=ww, sigma=s, tau=t)
+                for a in ALPHA_A for (s, t) in ALPHA_P for ww in ALPHA_W]
     if grid == "mesh":
-        return [dict(n=nn, nt=ss, alpha=alpha, window=w, sigma=sigma, tau=tau)
+        return [dict(n=nn, nt=ss, alpha=1e-3, window=25, sigma=4, tau=2)
                 for nn, ss in ((64, 4), (128, 8), (256, 16), (512, 32))]
     raise ValueError(grid)
 

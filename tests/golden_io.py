@@ -57,7 +57,7 @@ def _energy(c, shape, idx_last):
     return float(np.sum(w * np.abs(c) ** 2))
 
 
-def encode_v(v, tail_rel=1e-4, kmax=None):
+def encode_v(v, tail_rel=1e-4, kmax=None, prefix="v"):
     """Smallest cube K whose discarded tail is <= tail_rel ||v|| (or kmax); returns a dict."""
     v = np.asarray(v, dtype=np.float64)
     shape = v.shape[1:]
@@ -68,19 +68,20 @@ def encode_v(v, tail_rel=1e-4, kmax=None):
         cK, idx = _restrict(c, shape, K)
         tail2 = max(tot - _energy(cK, shape, idx[-1]), 0.0)
         if np.sqrt(tail2) <= tail_rel * np.sqrt(tot) or K == kmax:
-            return dict(v_K=np.int64(K), v_coef=cK.astype(np.complex64), v_tail=np.float64(np.sqrt(tail2)),
-                        v_norm=np.float64(np.sqrt(tot)), v_shape=np.array(v.shape))
+            return {f"{prefix}_K": np.int64(K), f"{prefix}_coef": cK.astype(np.complex64),
+                    f"{prefix}_tail": np.float64(np.sqrt(tail2)), f"{prefix}_norm": np.float64(np.sqrt(tot)),
+                    f"{prefix}_shape": np.array(v.shape)}
 
 
-def rel_l2_bound(v_gpu, g):
+def rel_l2_bound(v_gpu, g, prefix="v"):
     """Upper bound on ||v_gpu - v_ref|| / ||v_ref|| from the stored cube + tail (module docstring)."""
     v_gpu = np.asarray(v_gpu, dtype=np.float64)
     shape = v_gpu.shape[1:]
-    assert tuple(v_gpu.shape) == tuple(g["v_shape"])
-    K = int(g["v_K"])
+    assert tuple(v_gpu.shape) == tuple(g[f"{prefix}_shape"])
+    K = int(g[f"{prefix}_K"])
     c = _spec(v_gpu)
     cK, idx = _restrict(c, shape, K)
-    head = np.sqrt(_energy(cK - g["v_coef"].astype(np.complex128), shape, idx[-1]))
+    head = np.sqrt(_energy(cK - g[f"{prefix}_coef"].astype(np.complex128), shape, idx[-1]))
     tail_gpu = np.sqrt(max(float(np.sum(v_gpu * v_gpu)) - _energy(cK, shape, idx[-1]), 0.0))
     # complex64 storage rounding of the cube is ~6e-8 relative: negligible against 1e-3
-    return float(np.sqrt(head ** 2 + (tail_gpu + float(g["v_tail"])) ** 2) / float(g["v_norm"]))
+    return float(np.sqrt(head ** 2 + (tail_gpu + float(g[f"{prefix}_tail"])) ** 2) / float(g[f"{prefix}_norm"]))
