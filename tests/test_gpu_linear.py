@@ -79,10 +79,12 @@ def test_linear_ngmres_matches_oracle(n, alpha, p, w, iters):
     print("res ref", [f"{x:.3e}" for x in ref_res])
     assert err32 < 1e-3
     assert err < 1e-4 + 2 * spread
-    # residual histories: the fp64 oracle's until the fp32 storage effect sets in, the fp32-storage
-    # oracle's throughout
+    # residual histories: the fp64 oracle's to 1e-4 until fp32 storage sets in (k < 4), then within
+    # 1e-4 + twice the fp32-storage oracle's own deviation from it (two fp32 realisations of the same
+    # iteration differ by rounding order, not only by storage)
     np.testing.assert_allclose(res[:4], ref_res[:4], rtol=1e-4)
-    np.testing.assert_allclose(res, ref32_res, rtol=2e-3, atol=1e-6 * ref_res[0])
+    dev32 = max(abs(a - b) / b for a, b in zip(ref32_res, ref_res))
+    np.testing.assert_allclose(res, ref_res, rtol=1e-4 + 2 * dev32, atol=1e-6 * ref_res[0])
     if w >= iters:  # NGMRES(infinity) = GMRES: residuals never increase
         assert all(res[k + 1] <= res[k] * (1 + 1e-5) for k in range(iters))
         assert res[-1] < 0.2 * res[0]
