@@ -10,7 +10,9 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libtopt.so")
+# TOPT_LIB selects another build of the same ABI (tests: lib/libtopt_stress.so, the race-stress /
+# bounds-checked build); the default is the release library
+LIB_PATH = os.environ.get("TOPT_LIB") or os.path.join(HERE, "lib", "libtopt.so")
 
 NSCALARS = 16
 S_OBJ, S_DIST, S_REG, S_GRAD_INF, S_GS, S_SLV, S_SLS = range(7)

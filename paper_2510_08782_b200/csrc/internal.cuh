@@ -10,6 +10,29 @@
 
 namespace topt {
 
+// Race stress and bounds checks (libtopt_stress.so, built with -DTOPT_STRESS): at the
+// synchronisation points of the pipelined kernels a pseudo-random quarter of the warps sleeps for up
+// to ~1 us, reshuffling the interleavings a missing barrier or an early refill would expose, and ring /
+// window indices are checked (__trap on violation).  The release library compiles both to nothing.
+#ifdef TOPT_STRESS
+__device__ __forceinline__ void stress_point(unsigned salt) {
+  unsigned h = (blockIdx.x * 0x9E3779B1u) ^ ((threadIdx.x >> 5) * 0x85EBCA77u) ^ (salt * 0xC2B2AE3Du) ^
+               (unsigned)clock();
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  if ((h & 3u) == 0u) __nanosleep(32u + (h >> 22));
+}
+#define TOPT_STRESS_POINT(salt) ::topt::stress_point(salt)
+#define TOPT_DEVICE_CHECK(cond) \
+  do {                          \
+    if (!(cond)) __trap();      \
+  } while (0)
+#else
+#define TOPT_STRESS_POINT(salt) ((void)0)
+#define TOPT_DEVICE_CHECK(cond) ((void)0)
+#endif
+
 constexpr int kThreads = 256;
 constexpr int kMaxPartials = 1 << 17;  // per reduction slot
 constexpr int kNumSlots = 16;        // reduction slots in the partials buffer

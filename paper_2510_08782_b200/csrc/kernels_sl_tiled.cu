@@ -26,7 +26,6 @@
 #include <cmath>
 
 #include "internal.cuh"
-#include "tma.cuh"
 
 namespace topt {
 
@@ -92,6 +91,7 @@ __device__ __forceinline__ float gather_global(const Geom& g, const float* __res
     int r = (iz + g.zh - 1) % g.nzw;
     if (r < 0) r += g.nzw;
     iz = r - g.zh + 1;
+    TOPT_DEVICE_CHECK(iz - 1 >= -g.zh && iz + 2 < g.nz + g.zh);
   }
   float wx[4], wy[4], wz[4];
   lag4(dx - fx, wx);
@@ -175,11 +175,8 @@ constexpr int NZR = 16;                         // ring slots (power of two)
 static_assert(NZR >= 2 * H + (D + 1) * K, "ring too small");
 constexpr int PS = tiled::Cfg<H>::PS, PH = tiled::Cfg<H>::PH;
 constexpr int NF4 = PH * (tiled::XW / 4);  // float4 per plane
-#ifndef TOPT_SL_TMA
-#define TOPT_SL_TMA 0  // 1: ring filled by TMA bulk row copies on mbarriers (measured slower)
-#endif
-constexpr int NGRP = NZR / K;  // TMA: plane groups of K slots, one mbarrier each
-constexpr size_t SMEM = (size_t)NZR * PS * sizeof(float) + (TOPT_SL_TMA ? NGRP * sizeof(uint64_t) : 0);
+constexpr size_t SMEM = (size_t)NZR * PS * sizeof(float);
+static_assert(H % K == 0, "stages of K planes tile the halo");
 }  // namespace pipe
 
 #ifndef TOPT_TRACE2
@@ -213,87 +210,36 @@ __global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, T
   const float* __restrict__ in = a.in[0];
 
   auto psrc = [&](int pl) -> size_t { return (size_t)(g.zh ? pl + g.zh : (pl & (g.nz - 1))) * plane; };
-  // cp.async of input planes [pa, pb) into their ring slots (plane p -> slot p & (NZR-1))
-  auto load_planes = [&](int pa, int pb) {
-    const int n = (pb - pa) * pipe::NF4;
-    for (int i = threadIdx.x; i < n; i += 256) {
-      const int pl = pa + i / pipe::NF4, rem = i % pipe::NF4;
-      const int r = rem / (XW / 4), k = rem % (XW / 4);
-      const size_t src = psrc(pl) + (size_t)((y0 - H + r) & (g.ny - 1)) * g.nx + ((x0 - XH + 4 * k) & (g.nx - 1));
-      cp_async16(sm + (pl & (NZR - 1)) * PS + r * PW + 4 * k, in + src);
-    }
-  };
-  // steady-state stages load K planes = K * NF4 float4: thread t owns elements t + 256 j,
-  // whose plane offset, row / column source offset and smem offset are fixed
+  // ring fill by cp.async: a stage is K consecutive planes [pa, pa + K) (pa a multiple of K, so
+  // the planes are contiguous in the source, wrapped or halo'd, and land in one aligned slot group).
+  // Thread t owns float4 elements t + 256 j of the stage; their plane / row / column offsets are
+  // fixed, so per stage only the stage's source base and slot base are computed (32-bit offsets).
   constexpr int NJ = (K * pipe::NF4 + 255) / 256;
-  int jps[NJ];  // (plane offset << 16) | smem offset, or -1
-  unsigned jrc[NJ];
+  unsigned soff[NJ], goff[NJ];
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
-    const int i = threadIdx.x + 256 * j, rem = i % pipe::NF4;
+    const int i = threadIdx.x + 256 * j, jo = i / pipe::NF4, rem = i % pipe::NF4;
     const int r = rem / (XW / 4), k = rem % (XW / 4);
-    jps[j] = i < K * pipe::NF4 ? ((i / pipe::NF4) << 16) | (r * PW + 4 * k) : -1;
-    jrc[j] = (unsigned)(((y0 - H + r) & (g.ny - 1)) * g.nx + ((x0 - XH + 4 * k) & (g.nx - 1)));
+    soff[j] = (unsigned)(jo * PS + r * PW + 4 * k) * 4u;
+    goff[j] = (unsigned)jo * (unsigned)plane +
+              (unsigned)(((y0 - H + r) & (g.ny - 1)) * g.nx + ((x0 - XH + 4 * k) & (g.nx - 1)));
   }
+  const unsigned sm0 = (unsigned)__cvta_generic_to_shared(sm);
   auto load_stage = [&](int pa) {  // planes [pa, pa + K)
+    const float* src = in + psrc(pa);
+    const unsigned sb = sm0 + (unsigned)((pa & (NZR - 1)) * PS) * 4u;
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-      if (jps[j] < 0) continue;
-      const int pl = pa + (jps[j] >> 16);
-      cp_async16(sm + (pl & (NZR - 1)) * PS + (jps[j] & 0xffff), in + psrc(pl) + jrc[j]);
-    }
+    for (int j = 0; j < NJ; ++j)
+      if (threadIdx.x + 256 * j < K * pipe::NF4) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sb + soff[j]), "l"(src + goff[j]));
   };
 
   const int nst = ZC / K;
-#if TOPT_SL_TMA
-  // TMA ring fill: the K planes of a group (K x PH rows of XW floats, periodic in x and y) are
-  // copied by warp 0 with bulk copies completing on the group's mbarrier; stage s reads groups
-  // s-1, s, s+1 (H == K) and, after its barrier, warp 0 refills the group stage s-1 released with
-  // group s+2.  Every thread tracks the groups' phase parities in `phase`.
-  static_assert(H == K && pipe::D == 1, "TMA ring: halo of one group, prefetch distance one stage");
-  (void)load_planes;
-  (void)load_stage;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + NZR * PS);
-  auto tma_group = [&](int pa) {  // warp 0: planes [pa, pa + K)
-    uint64_t* bar = bars + ((pa & (NZR - 1)) / K);
-    if (threadIdx.x == 0) tma::mbar_arrive_expect_tx(bar, K * pipe::PH * XW * 4);
-    __syncwarp();
-    for (int q = threadIdx.x; q < K * pipe::PH; q += 32) {
-      const int pl = pa + q / pipe::PH, r = q % pipe::PH;
-      float* dst = sm + (pl & (NZR - 1)) * PS + r * PW;
-      const float* row = in + psrc(pl) + (size_t)((y0 - H + r) & (g.ny - 1)) * g.nx;
-      for (int c = 0; c < XW;) {  // columns x0 - XH .. x0 + TX + XH - 1: up to 3 contiguous runs
-        const int gx = (x0 - XH + c) & (g.nx - 1);
-        const int len = min(XW - c, g.nx - gx);
-        tma::bulk_g2s(dst + c, row + gx, (unsigned)len * 4u, bar);
-        c += len;
-      }
-    }
-  };
-  unsigned phase = 0;
-  auto wait_group = [&](int pa) {
-    const int gi = (pa & (NZR - 1)) / K;
-    tma::mbar_wait(bars + gi, (phase >> gi) & 1u);
-    phase ^= 1u << gi;
-  };
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < pipe::NGRP; ++i) tma::mbar_init(bars + i, 1);
-    tma::fence_mbar_init();
-  }
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    tma_group(z0 - H);
-    tma_group(z0);
-    tma_group(z0 + K);
-  }
-#else
-  load_planes(z0 - H, z0 + K + H);  // stage 0
+  for (int p = z0 - H; p < z0 + K + H; p += K) load_stage(p);  // stage 0's planes
   cp_commit();
   for (int u = 1; u < pipe::D; ++u) {  // stages 1 .. D-1
     if (u < nst) load_stage(z0 + u * K + H);
     cp_commit();
   }
-#endif
 
   const size_t gi0 = (size_t)z0 * plane + (size_t)(y0 + ty) * g.nx + x0 + tx;
   // per-thread stream bases; offsets from them fit 32 bits (3F < 2^32 for every supported grid)
@@ -317,20 +263,12 @@ __global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, T
   for (int st = 0; st < nst; ++st) {
     // one barrier per stage: after it every thread has finished stage st-1, whose oldest
     // K slots (planes needed by no later stage, NZR >= 2H + (D+1)K) take stage st+D's planes
-#if TOPT_SL_TMA
-    if (st == 0) {
-      wait_group(z0 - H);
-      wait_group(z0);
-    }
-    wait_group(z0 + (st + 1) * K);
-    __syncthreads();
-    if (threadIdx.x < 32 && st + 1 < nst) tma_group(z0 + (st + 2) * K);
-#else
+    TOPT_STRESS_POINT(st * 3 + 11);
     cp_wait<pipe::D - 1>();
     __syncthreads();
     if (st + pipe::D < nst) load_stage(z0 + (st + pipe::D) * K + H);
     cp_commit();
-#endif
+    TOPT_STRESS_POINT(st * 3 + 12);
 #pragma unroll 1
     for (int j = 0; j < K; ++j) {
       const int zi = st * K + j, z = z0 + zi;
@@ -340,6 +278,9 @@ __global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, T
       const float fx = floorf(dx), fy = floorf(dy), fz = floorf(dz);
       const int ix = (int)fx, iy = (int)fy, iz = (int)fz;
       float r;
+      // resident ring planes during stage st: [z0 + st K - H, z0 + st K + K + H)
+      TOPT_DEVICE_CHECK(!(iz >= -H + 1 && iz <= H - 2) ||
+                        (z + iz - 1 >= z0 + st * K - H && z + iz + 2 < z0 + st * K + K + H));
       const bool inr = !(ix < -XH + 1 || ix > XH - 2 || iy < -H + 1 || iy > H - 2 || iz < -H + 1 || iz > H - 2);
 #if TOPT_SL_XWIN
       // x-window path (warp-uniform): when the warp's x floors take exactly two values
@@ -410,9 +351,7 @@ __global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, T
       }
     }
   }
-#if !TOPT_SL_TMA
   cp_wait<0>();
-#endif
 
   if (MODE == M_LAST) {
     __shared__ double red[8];
@@ -602,7 +541,10 @@ __global__ void __launch_bounds__(256, 2) k_sl_trace(Geom g, int ZC, TileArgs a)
 // 250.  Otherwise the pair takes the per-point paths of k_sl_trace.  The 8-slot plane ring is
 // filled with cp.async, two planes per step, one barrier per pair.
 // =====================================================================================
-__global__ void __launch_bounds__(256, 2) k_sl_trace2(Geom g, int ZC, TileArgs a) {
+#ifndef TOPT_TRACE_MINB
+#define TOPT_TRACE_MINB 2
+#endif
+__global__ void __launch_bounds__(256, TOPT_TRACE_MINB) k_sl_trace2(Geom g, int ZC, TileArgs a) {
   using namespace tiled;
   constexpr int HALO = 2, NF = 3, NZR = 8;
   constexpr int PS = Cfg<HALO>::PS, PH = Cfg<HALO>::PH, NF4 = PH * (XW / 4);
@@ -634,22 +576,23 @@ __global__ void __launch_bounds__(256, 2) k_sl_trace2(Geom g, int ZC, TileArgs a
   double vs0 = 0.0, vs1 = 0.0, vs2 = 0.0;
   const size_t gi0 = (size_t)z0 * plane + (size_t)(y0 + ty) * g.nx + x0 + tx;
   const int rbase = (ty - 2 + HALO) * PW + tx - 2 + XH;
-  // (forward, adjoint) weights of one point on window nodes -2..2 per axis
+  // (forward, adjoint) weights of one point on window nodes -2..2 per axis.  The two feet of a
+  // point are displaced by -c/2 and +c/2 (|c/2| < 1): their fractional offsets are t and 1 - t and
+  // their stencils mirror images in the 5-node window, so the forward weights are the adjoint
+  // 5-vector reversed (w_k(1 - t) = w_{3-k}(t) for the Lagrange basis on -1..2): one lag4 per axis
   auto weights = [&](const float cc[3], float2 (&W)[3][5]) {
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-      const float dF = 0.5f * -1.0f * cc[ax], dA = 0.5f * 1.0f * cc[ax];
-      const float fF = floorf(dF), fA = floorf(dA);
-      float wF[4], wA[4];
-      lag4(dF - fF, wF);
+      const float dA = 0.5f * cc[ax];
+      const float fA = floorf(dA);
+      float wA[4];
       lag4(dA - fA, wA);
-      const bool sF = fF == 0.0f, sA = fA == 0.0f;
+      const bool sA = fA == 0.0f;  // adjoint stencil at window offsets 1..4 (else 0..3)
+      float a5[5];
 #pragma unroll
-      for (int k = 0; k < 5; ++k) {
-        const float f0 = k < 4 ? wF[k] : 0.0f, f1 = k > 0 ? wF[k - 1] : 0.0f;
-        const float a0 = k < 4 ? wA[k] : 0.0f, a1 = k > 0 ? wA[k - 1] : 0.0f;
-        W[ax][k] = make_float2(sF ? f1 : f0, sA ? a1 : a0);
-      }
+      for (int k = 0; k < 5; ++k) a5[k] = sA ? (k > 0 ? wA[k - 1] : 0.0f) : (k < 4 ? wA[k] : 0.0f);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) W[ax][k] = make_float2(a5[4 - k], a5[k]);
     }
   };
   // per-point, per-side path (k_sl_trace's): stencil at the foot's own floors
@@ -684,6 +627,7 @@ __global__ void __launch_bounds__(256, 2) k_sl_trace2(Geom g, int ZC, TileArgs a
 #pragma unroll 1
   for (int zi = 0; zi < ZC; zi += 2) {
     const int z = z0 + zi;
+    TOPT_STRESS_POINT(zi + 21);
     cp_wait<0>();
     __syncthreads();  // planes z-2 .. z+3 resident; everyone is done with the previous pair
     if (zi + 2 < ZC) load_planes(z + 2 + HALO, z + 4 + HALO);  // over planes z-4, z-3

@@ -513,7 +513,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_rds_tma(Geom g, int axis, const
   for (int k = 0; k < total; ++k) {
     const int slot = k & 1, j = k % J;
     // slot (k+1)&1 held slice k-1: every thread left it at the end-of-slice barrier below
+    TOPT_STRESS_POINT(k * 5 + 31);
     if (threadIdx.x == 0 && k + 1 < total) issue(k + 1);
+    TOPT_STRESS_POINT(k * 5 + 32);
     tma::mbar_wait(bars + slot, (unsigned)(k >> 1) & 1u);
     float2* tp = reinterpret_cast<float2*>(tiles + (2 * slot) * TILE);
     const float2* tl = reinterpret_cast<const float2*>(tiles + (2 * slot + 1) * TILE);
@@ -560,12 +562,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_rds_tma(Geom g, int axis, const
         acc[e] = make_float2(0.f, 0.f);
       }
     }
+    TOPT_STRESS_POINT(k * 5 + 33);
     __syncthreads();  // slot k&1 (tiles and scratch) free for slice k+2
   }
 }
 
 #ifndef TOPT_RDS_TMA
 #define TOPT_RDS_TMA 1
+#endif
+#ifndef TOPT_RDS_TMA_J1
+#define TOPT_RDS_TMA_J1 0  // 1: div v passes TMA-staged too (measured slower: 1.63 vs 2.09 TB/s)
 #endif
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -640,7 +646,8 @@ static void deriv_dispatch(const Geom& g, int axis, const DerivArgs& a, const De
     k_rdx<N><<<blocks, kThreads, sm, st>>>(g, a.psi, a.psi_stride, a.lam, a.lam_stride, w, a.J, a.beta, a.out,
                                             (int)groups);
   } else if (a.J == 1) {
-    rds_launch<N, 8>(g, axis, a, w, st);   // single field (div v): occupancy first
+    // single field (div v): the TMA-staged pass pipelines across work items; else occupancy first
+    if (!(TOPT_RDS_TMA_J1 && rds_tma_launch<N>(g, axis, a, w, st))) rds_launch<N, 8>(g, axis, a, w, st);
   } else {
     // time-slice sums: one smem exchange per FFT; at N >= 512 (one resident block per SM)
     // the tiles of the next slice are prefetched with cp.async (measured: +7% at 512^3,
@@ -1030,6 +1037,7 @@ __global__ void __launch_bounds__(kThreads, TOPT_RZ_MINB) k_rzmerge(Geom g, int 
 #if TOPT_RZ_PF
     // this item's lines were staged by the previous iteration (or the prologue); take them,
     // free the staging tiles and start the next item's copies before the transforms
+    TOPT_STRESS_POINT(item + 41);
     cp_wait0_f();
     __syncthreads();
 #pragma unroll

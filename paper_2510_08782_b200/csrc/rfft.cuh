@@ -132,6 +132,7 @@ __device__ __forceinline__ void rf_stage(C (&a)[E], C* line, int t, const C* tw)
 #pragma unroll
     for (int e = 0; e < E; ++e) a[e] = o[e];
   } else {
+    TOPT_STRESS_POINT(NS * 17 + 1);
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       const int j = t + b * T;
@@ -140,6 +141,7 @@ __device__ __forceinline__ void rf_stage(C (&a)[E], C* line, int t, const C* tw)
       for (int q = 0; q < R; ++q) line[rf_idx<LS>(base + q * NS)] = o[b + q * B];
     }
     rf_sync<WARP>();
+    TOPT_STRESS_POINT(NS * 17 + 2);
 #pragma unroll
     for (int e = 0; e < E; ++e) a[e] = line[rf_idx<LS>(t + T * e)];
     rf_sync<WARP>();
