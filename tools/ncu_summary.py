@@ -20,7 +20,7 @@ KEYS = [
 def main(path, top=8):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr = rows[0]
+    hdr, units = rows[0], rows[1]  # the raw page's second row holds each metric's unit
     res = []
     for r in rows[2:]:
         name = r[hdr.index("Kernel Name")]
@@ -28,8 +28,9 @@ def main(path, top=8):
         d = {}
         for k in KEYS:
             if k in hdr:
-                d[k] = r[hdr.index(k)]
-                print(f"   {k:70s} {r[hdr.index(k)]}")
+                i = hdr.index(k)
+                d[k] = (r[i], units[i])
+                print(f"   {k:70s} {r[i]:>16s} {units[i]}")
         st = [(hdr[i], r[i]) for i in range(len(hdr))
               if hdr[i].startswith("smsp__average_warps_issue_stalled_") and hdr[i].endswith("_per_issue_active.ratio")
               and r[i]]
