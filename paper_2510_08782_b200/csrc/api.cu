@@ -212,7 +212,14 @@ topt_status topt_create(const topt_params* p, int32_t rank, int32_t world, const
   c->ws_need = b * c->comm.nloc;
   upload_twiddles();
   if (c->comm.P == 1) {  // side stream for v-only work (eval_gradient), see eval_gradient
-    cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+#ifndef TOPT_SIDE_PRIO
+#define TOPT_SIDE_PRIO 1
+#endif
+    // high priority: the block scheduler hands SMs freed by the SL grids to the side stream's blocks
+    // first, so div v and the fp64 v transforms interleave with the sweeps instead of trailing them
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, TOPT_SIDE_PRIO ? hi : lo);
     cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->ev_div, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->ev_u, cudaEventDisableTiming);

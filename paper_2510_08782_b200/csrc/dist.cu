@@ -16,6 +16,7 @@
 #include <cstdio>
 
 #include "ctx.cuh"
+#include "window.h"
 
 namespace topt {
 
@@ -176,21 +177,6 @@ bool comm_halo(topt_ctx* c, const std::vector<float*>& base, int nf, size_t fstr
 // nf fields: field f of slab s at src[s] + f * fs floats (its LOCAL planes), written to slab s's
 // win + f * (nzl + 2 zw) plane floats.  Runs of consecutive planes with one owner move as one
 // copy (emulated) or one ncclSend / ncclRecv pair, issued in window order on both sides.
-namespace {
-struct Run { int q, lp, w, len; };
-std::vector<Run> window_runs(int z0, int nzl, int nzg, int zw) {
-  std::vector<Run> runs;
-  const int W = nzl + 2 * zw;
-  for (int w = 0; w < W;) {
-    int zg = (z0 - zw + w) % nzg;
-    if (zg < 0) zg += nzg;
-    const int q = zg / nzl, lp = zg - q * nzl, len = std::min(W - w, nzl - lp);
-    runs.push_back({q, lp, w, len});
-    w += len;
-  }
-  return runs;
-}
-}  // namespace
 
 bool comm_window(topt_ctx* c, const std::vector<const float*>& src, size_t fs, int nf, int zw, cudaStream_t st) {
   const Comm& cm = c->comm;
@@ -200,7 +186,7 @@ bool comm_window(topt_ctx* c, const std::vector<const float*>& src, size_t fs, i
   if (zw > c->hcap) return false;
   if (cm.emulated()) {
     for (int r = 0; r < cm.P; ++r)
-      for (const Run& u : window_runs(r * nzl, nzl, nzg, zw))
+      for (const WindowRun& u : window_runs(r * nzl, nzl, nzg, zw))
         for (int f = 0; f < nf; ++f)
           cudaMemcpyAsync(c->slabs[r].win + f * ws + (size_t)u.w * pl, src[u.q] + f * fs + (size_t)u.lp * pl,
                           (size_t)u.len * pl * 4, cudaMemcpyDeviceToDevice, st);
@@ -209,7 +195,7 @@ bool comm_window(topt_ctx* c, const std::vector<const float*>& src, size_t fs, i
 #ifdef TOPT_WITH_NCCL
   const int me = s0.index;
   float* win = c->slabs[0].win;
-  for (const Run& u : window_runs(me * nzl, nzl, nzg, zw))  // my own planes
+  for (const WindowRun& u : window_runs(me * nzl, nzl, nzg, zw))  // my own planes
     if (u.q == me)
       for (int f = 0; f < nf; ++f)
         cudaMemcpyAsync(win + f * ws + (size_t)u.w * pl, src[0] + f * fs + (size_t)u.lp * pl, (size_t)u.len * pl * 4,
@@ -217,13 +203,13 @@ bool comm_window(topt_ctx* c, const std::vector<const float*>& src, size_t fs, i
   bool ok = nccl_ok(ncclGroupStart(), "ncclGroupStart");
   for (int r = 0; r < cm.P && ok; ++r) {
     if (r == me) continue;
-    for (const Run& u : window_runs(r * nzl, nzl, nzg, zw))  // what rank r needs from me
+    for (const WindowRun& u : window_runs(r * nzl, nzl, nzg, zw))  // what rank r needs from me
       if (u.q == me)
         for (int f = 0; f < nf; ++f)
           ok &= nccl_ok(ncclSend(src[0] + f * fs + (size_t)u.lp * pl, (size_t)u.len * pl * 4, ncclChar, r, cm.nccl, st),
                         "ncclSend");
   }
-  for (const Run& u : window_runs(me * nzl, nzl, nzg, zw))  // what I need from the others
+  for (const WindowRun& u : window_runs(me * nzl, nzl, nzg, zw))  // what I need from the others
     if (u.q != me)
       for (int f = 0; f < nf && ok; ++f)
         ok &= nccl_ok(ncclRecv(win + f * ws + (size_t)u.w * pl, (size_t)u.len * pl * 4, ncclChar, u.q, cm.nccl, st),
