@@ -470,11 +470,15 @@ static void rds_pf_launch(const Geom& g, int axis, const DerivArgs& a, const Der
 struct TmaDeriv {
   CUtensorMap psi, lam;  // 4D (x, y, z, slice), box (2 TXC, N or 1, 1 or N, 1) capped at 256 positions
 };
+#ifndef TOPT_RDS_TMA_THREADS
+#define TOPT_RDS_TMA_THREADS 128  // block size: 128 threads, 64 KB of tiles, 3 blocks per SM (256: 1 block, -6%)
+#endif
+constexpr int kRdsThreads = TOPT_RDS_TMA_THREADS;
 template <int N>
-__global__ void __launch_bounds__(kThreads, 1) k_rds_tma(Geom g, int axis, const __grid_constant__ TmaDeriv tm,
-                                                         bool has_lam, DerivWeights w, int J, float beta,
-                                                         float* __restrict__ out, int nitems) {
-  constexpr int E = Ev<N, 16>::v, T = N / E, TXC = kThreads / T;
+__global__ void __launch_bounds__(kRdsThreads, kRdsThreads == 256 ? 1 : 3) k_rds_tma(
+    Geom g, int axis, const __grid_constant__ TmaDeriv tm, bool has_lam, DerivWeights w, int J, float beta,
+    float* __restrict__ out, int nitems) {
+  constexpr int E = Ev<N, 16>::v, T = N / E, TXC = kRdsThreads / T;
   constexpr int TILE = N * 2 * TXC;  // floats per staged tile
   constexpr int BOX = N < 256 ? N : 256;
   extern __shared__ __align__(128) float smf[];
@@ -602,8 +606,8 @@ static bool slice_map(CUtensorMap* m, const float* base, const Geom& g, size_t s
 }
 template <int N>
 static bool rds_tma_launch(const Geom& g, int axis, const DerivArgs& a, const DerivWeights& w, cudaStream_t st) {
-  constexpr int T = N / Ev<N, 16>::v, TXC = kThreads / T;
-  if (!TOPT_RDS_TMA || N < 128 || N > 1024 || 2 * TXC > g.nx || g.nx % (2 * TXC)) return false;
+  constexpr int T = N / Ev<N, 16>::v, TXC = kRdsThreads / T;
+  if (!TOPT_RDS_TMA || N < 128 || N > 1024 || 2 * TXC > g.nx || g.nx % (2 * TXC) || 2 * TXC * 4 < 16) return false;
   if (((uintptr_t)a.psi | (uintptr_t)(a.lam ? a.lam : a.psi)) & 15) return false;
   if ((a.psi_stride | (a.lam ? a.lam_stride : 0)) & 3) return false;
   TmaDeriv tm{};
@@ -613,8 +617,8 @@ static bool rds_tma_launch(const Geom& g, int axis, const DerivArgs& a, const De
   const size_t sm = 4 * (size_t)N * 2 * TXC * sizeof(float) + 2 * sizeof(uint64_t);
   const int outer = axis == 1 ? g.nz : g.ny;
   const long long items = (long long)(g.nx / (2 * TXC)) * outer;
-  const int blocks = persistent_blocks(k_rds_tma<N>, kThreads, sm, items);
-  k_rds_tma<N><<<blocks, kThreads, sm, st>>>(g, axis, tm, a.lam != nullptr, w, a.J, a.beta, a.out, (int)items);
+  const int blocks = persistent_blocks(k_rds_tma<N>, kRdsThreads, sm, items);
+  k_rds_tma<N><<<blocks, kRdsThreads, sm, st>>>(g, axis, tm, a.lam != nullptr, w, a.J, a.beta, a.out, (int)items);
   return true;
 }
 
