@@ -6,7 +6,8 @@ structure as tests/test_gpu_fullsize.py at 256^3, for all three models:
   * the body force b = sum_j w_j lam^j grad m^j (continuity: -sum w_j pi^j grad lam^j, R8; R10);
   * g = alpha L v + b (incompressible: P_L(...), R9) and s = -(alpha L~)^{-1} g (P:134, P:172);
   * dist, reg, <g, s>_h and ||g||_inf from the GPU's fields.
-Whole fields, every time slice.  Cites: P:105-121 (gradient / adjoint), P:126 (trapezoid), P:136 (SL)."""
+Also the feet and every forward step (fed the GPU's m^j).  Whole fields, every time slice; the
+configs' own grids for configs 2 (64^3, H1) and 3 (128^3, incompressible).  Cites: P:105-121 (gradient / adjoint), P:126 (trapezoid), P:136 (SL)."""
 import numpy as np
 import pytest
 import torch
@@ -37,20 +38,32 @@ def _run(cfg, n, model):
     g, s, sc = t.eval_gradient(dev(d["m0"]), dev(d["m1"]), dev(d["v"]))
     lam, b = t.adjoint()
     traj = t.forward(dev(d["m0"]), dev(d["v"]))
+    df, da = t.feet(dev(d["v"]))
     torch.cuda.synchronize()
-    return d, dict(g=host(g), s=host(s), sc=t.scalars_dict(sc), lam=host(lam), b=host(b), m=host(traj))
+    return d, dict(g=host(g), s=host(s), sc=t.scalars_dict(sc), lam=host(lam), b=host(b), m=host(traj),
+                   df=host(df), da=host(da))
 
 
-@pytest.mark.parametrize("cfg,n", GRIDS)
-@pytest.mark.parametrize("model", [0, 1, 2])
+CASES = [(c, n, m) for c, n in GRIDS for m in (0, 1, 2)]
+CASES += [(2, (64, 64, 64), 0),      # config 2 at its native grid and model (H1)
+          (3, (128, 128, 128), 2)]   # config 3 at its native grid and model (Leray, H2)
+
+
+@pytest.mark.parametrize("cfg,n,model", CASES)
 def test_operator_chain(cfg, n, model):
     d, r = _run(cfg, n, model)
     grid, nt, v = d["grid"], d["nt"], d["v"]
     lam, m = r["lam"], r["m"]
+    # feet (R5, R6) and every forward step fed the GPU's m^j (continuity: Heun factor, R7)
+    rf, ra = transport.feet(grid, v, nt)
+    assert rel_l2(r["df"], rf) < TOL and rel_l2(r["da"], ra) < TOL, "feet"
+    Ef = transport.source_factor_forward_continuity(grid, v, rf, nt) if model == 1 else 1.0
+    assert np.array_equal(m[0], d["m0"])
+    for j in range(nt):
+        assert rel_l2(m[j + 1], interp(m[j], rf) * Ef) < TOL, ("forward step", j)
     # lam^S: fp32 subtraction of fp32 operands is the correctly rounded exact difference
     np.testing.assert_array_equal(lam[nt], (d["m1"] - m[nt]).astype(np.float32))
     # adjoint steps
-    _, ra = transport.feet(grid, v, nt)
     E = transport.source_factor_adjoint_advection(grid, v, ra, nt) if model == 0 else 1.0
     for j in range(nt - 1, -1, -1):
         ref = interp(lam[j + 1], ra) * E
