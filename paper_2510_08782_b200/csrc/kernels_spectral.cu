@@ -991,7 +991,16 @@ __global__ void __launch_bounds__(kThreads, TOPT_RZ_MINB) k_rzmerge(Geom g, int 
   extern __shared__ __align__(16) unsigned char smraw[];
   const int c = threadIdx.x % TXC, t = threadIdx.x / TXC;
   double2* lbd = reinterpret_cast<double2*>(smraw) + c * R::STRIDE;  // fp64 line scratch
-  float2* lbf = reinterpret_cast<float2*>(smraw) + c * R::STRIDE;    // fp32 (same region, used after)
+  // fp32 line scratch (same region, used after the fp64 transform).  Its column stride is chosen apart
+  // from the fp64 one: at STRIDE (273 float2 = 546 words = 2 mod 32) the 8 columns of a half-warp
+  // phase sit 2 words apart, exactly where the neighbouring position of the next t lands (bank
+  // conflicts); TOPT_RZ_FSTRIDE float2 per column (274 = 548 words = 4 mod 32) separates them
+#ifndef TOPT_RZ_FSTRIDE
+#define TOPT_RZ_FSTRIDE 274
+#endif
+  constexpr int SF = (N == 256 && TOPT_RZ_FSTRIDE >= R::STRIDE) ? TOPT_RZ_FSTRIDE : R::STRIDE;
+  static_assert(SF * sizeof(float2) <= R::STRIDE * sizeof(double2), "fp32 scratch inside the fp64 one");
+  float2* lbf = reinterpret_cast<float2*>(smraw) + c * SF;
   double2 twd[R::NTW];
   float2 twf[R::NTW];
   rf_twiddles<N, E>(twd, t);

@@ -100,8 +100,16 @@ __device__ __forceinline__ void rf_sync() {
 // scratch addressing of the stage-boundary exchange: LS == 0 -> line[fft_pad(i)] (a padded line of
 // its own); LS > 0 -> line[i * LS] (lines interleaved with stride LS: a [position][line] tile, e.g. a
 // TMA-staged input tile reused as scratch once its values are in registers)
+// In the interleaved form a half-warp phase of 64-bit accesses holds 16 / LS positions; the radix-16
+// write pattern puts two of them 16 positions apart (same parity: same banks), so position i is
+// stored at i ^ bit4(i) — a bijection that gives the two different parities.
+#ifndef TOPT_RF_SWZ
+#define TOPT_RF_SWZ 1
+#endif
 template <int LS>
-__device__ __forceinline__ int rf_idx(int i) { return LS == 0 ? fft_pad(i) : i * LS; }
+__device__ __forceinline__ int rf_idx(int i) {
+  return LS == 0 ? fft_pad(i) : (TOPT_RF_SWZ ? (i ^ ((i >> 4) & 1)) : i) * LS;
+}
 
 template <int N, int E, int NS, int OFF, bool INV, bool WARP, bool FULL, int LS, typename C>
 __device__ __forceinline__ void rf_stage(C (&a)[E], C* line, int t, const C* tw) {
