@@ -1,0 +1,2 @@
+python -m pytest tests -q -m gpu -x -p no:cacheprovider -k "operators or fullsize or maxsize or parity or slabs or edge" > gpurun_out/r2_pytest18.log 2>&1; echo "rc=$?" >> gpurun_out/r2_pytest18.log
+bash tools/ab_build.sh "" "-DTOPT_SL_QUAD=0" > gpurun_out/r2_ab18.txt 2>&1
