@@ -368,288 +368,6 @@ __global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, T
 }
 
 // =====================================================================================
-// SL step with register reuse across the K = 4 planes of a stage (k_sl_quad, MODE STEP).
-// Same ring, pipeline and arithmetic as k_sl_pipe, but a thread computes the 4 points of its
-// column in the stage at once.  When those 4 feet share their floor offsets (ix, iy, iz) — 81% of
-// the lanes at 256^3 config 4 — their 4 x 4 x 4 stencils are the same 16 (x, y) columns in 7
-// consecutive planes, so each loaded value serves up to 4 points: 7 planes x 4 rows x W columns
-// (W = 4, or 5 at lane-uniform offsets when the lanes' floors span two values: no bank conflicts)
-// = 112-140 loads per 4 points instead of 256-320.  Points are paired in fp32x2 FMAs ((0,1) over
-// planes 0..4, (2,3) over planes 2..6, zero z weights outside a point's 4 planes).  Lanes whose
-// points do not share floors, and warps whose lanes' x floors span more than two values, push
-// their points to a per-warp queue in shared memory, evaluated after the quad pass by the
-// per-point path (x window / per-lane / L1) with full warps: the ring still holds the stage.
-// =====================================================================================
-#ifndef TOPT_SL_QUAD
-#define TOPT_SL_QUAD 0
-#endif
-#ifndef TOPT_SL_QUAD_MINB
-#define TOPT_SL_QUAD_MINB 2
-#endif
-namespace quad {
-constexpr int QCAP = 4 * 32;  // queue entries per warp (every point of the stage)
-constexpr size_t SMEM = pipe::SMEM + (size_t)8 * QCAP * 5 * sizeof(float);
-}  // namespace quad
-
-template <bool HAS_E>
-__global__ void __launch_bounds__(256, TOPT_SL_QUAD_MINB) k_sl_quad(Geom g, int ZC, TileArgs a) {
-  using namespace tiled;
-  using pipe::H;
-  using pipe::K;
-  using pipe::NZR;
-  using pipe::PS;
-  static_assert(K == 4 && H == 4, "quad: stages of 4 planes, halo 4");
-  extern __shared__ __align__(16) float sm[];  // [NZR][PH][PW], then the queues
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int tilesx = g.nx / TX, tilesy = g.ny / TY;
-  int bid = blockIdx.x;
-  const int bx = bid % tilesx;
-  bid /= tilesx;
-  const int by = bid % tilesy;
-  bid /= tilesy;
-  const int z0 = bid * ZC;
-  const int x0 = bx * TX, y0 = by * TY;
-  const size_t plane = (size_t)g.nx * g.ny;
-  const float* __restrict__ in = a.in[0];
-  // per-warp queue: [QCAP] entries of (code = k << 5 | lane, dx, dy, dz, E) as 5 arrays
-  float* qbase = sm + NZR * PS + (size_t)ty * quad::QCAP * 5;
-  int* qcode = reinterpret_cast<int*>(qbase);
-  float* qdx = qbase + quad::QCAP;
-  float* qdy = qdx + quad::QCAP;
-  float* qdz = qdy + quad::QCAP;
-  float* qE = qdz + quad::QCAP;
-
-  auto psrc = [&](int pl) -> size_t { return (size_t)(g.zh ? pl + g.zh : (pl & (g.nz - 1))) * plane; };
-  constexpr int NJ = (K * pipe::NF4 + 255) / 256;
-  unsigned soff[NJ], goff[NJ];
-#pragma unroll
-  for (int j = 0; j < NJ; ++j) {
-    const int i = threadIdx.x + 256 * j, jo = i / pipe::NF4, rem = i % pipe::NF4;
-    const int r = rem / (XW / 4), k = rem % (XW / 4);
-    soff[j] = (unsigned)(jo * PS + r * PW + 4 * k) * 4u;
-    goff[j] = (unsigned)jo * (unsigned)plane +
-              (unsigned)(((y0 - H + r) & (g.ny - 1)) * g.nx + ((x0 - XH + 4 * k) & (g.nx - 1)));
-  }
-  const unsigned sm0 = (unsigned)__cvta_generic_to_shared(sm);
-  auto load_stage = [&](int pa) {  // planes [pa, pa + K)
-    const float* src = in + psrc(pa);
-    const unsigned sb = sm0 + (unsigned)((pa & (NZR - 1)) * PS) * 4u;
-#pragma unroll
-    for (int j = 0; j < NJ; ++j)
-      if (threadIdx.x + 256 * j < K * pipe::NF4)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sb + soff[j]), "l"(src + goff[j]));
-  };
-  const int nst = ZC / K;
-  for (int p = z0 - H; p < z0 + K + H; p += K) load_stage(p);
-  cp_commit();
-
-  const size_t gi0 = (size_t)z0 * plane + (size_t)(y0 + ty) * g.nx + x0 + tx;
-  const float* __restrict__ pd = a.delta + gi0;
-  const float* __restrict__ pE = HAS_E ? a.E + gi0 : nullptr;
-  float* __restrict__ pout = a.out[0] + gi0;
-  const unsigned F32 = (unsigned)g.F, P32 = (unsigned)plane;
-
-  // the per-point path of k_sl_pipe for queue entries (all 32 lanes call it; `valid` masks)
-  auto single = [&](bool valid, int lx, int z, float dx, float dy, float dz) -> float {
-    const float fx = floorf(dx), fy = floorf(dy), fz = floorf(dz);
-    const int ix = (int)fx, iy = (int)fy, iz = (int)fz;
-    const bool inr = !(ix < -XH + 1 || ix > XH - 2 || iy < -H + 1 || iy > H - 2 || iz < -H + 1 || iz > H - 2);
-    const int mn = __reduce_min_sync(0xffffffffu, valid ? ix : 1 << 20);
-    const int mx = __reduce_max_sync(0xffffffffu, valid ? ix : -(1 << 20));
-    float r = 0.0f;
-    if (mx == mn + 1 && __all_sync(0xffffffffu, inr || !valid)) {
-      if (valid) {
-        float wx[4], wy[4], wz[4];
-        lag4(dx - fx, wx);
-        lag4(dy - fy, wy);
-        lag4(dz - fz, wz);
-        const bool sh = ix != mn;
-        float w5[5];
-#pragma unroll
-        for (int k = 0; k < 5; ++k) w5[k] = sh ? (k > 0 ? wx[k - 1] : 0.0f) : (k < 4 ? wx[k] : 0.0f);
-        const int p0 = z + iz - 1;
-        const int ro = (ty + iy - 1 + H) * PW + lx + mn - 1 + XH;
-        const float* s0 = sm + ((p0) & (NZR - 1)) * PS + ro;
-        const float* s1 = sm + ((p0 + 1) & (NZR - 1)) * PS + ro;
-        const float* s2 = sm + ((p0 + 2) & (NZR - 1)) * PS + ro;
-        const float* s3 = sm + ((p0 + 3) & (NZR - 1)) * PS + ro;
-        float2 lo = make_float2(0.f, 0.f), hi = lo;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          float2 r01 = make_float2(0.f, 0.f), r23 = r01;
-#pragma unroll
-          for (int k = 0; k < 5; ++k) {
-            const int oo = b * PW + k;
-            const float2 w = make_float2(w5[k], w5[k]);
-            r01 = __ffma2_rn(w, make_float2(s0[oo], s1[oo]), r01);
-            r23 = __ffma2_rn(w, make_float2(s2[oo], s3[oo]), r23);
-          }
-          const float2 wb = make_float2(wy[b], wy[b]);
-          lo = __ffma2_rn(wb, r01, lo);
-          hi = __ffma2_rn(wb, r23, hi);
-        }
-        r = fmaf(wz[3], hi.y, fmaf(wz[2], hi.x, fmaf(wz[1], lo.y, wz[0] * lo.x)));
-      }
-    } else if (valid) {
-      if (!inr) {
-        r = gather_global(g, in, x0 + lx, y0 + ty, z, dx, dy, dz);
-      } else {
-        float wx[4], wy[4], wz[4];
-        lag4(dx - fx, wx);
-        lag4(dy - fy, wy);
-        lag4(dz - fz, wz);
-        const int p0 = z + iz - 1;
-        gather_smem<1, 0>(sm, [&](int c) { return ((p0 + c) & (NZR - 1)) * PS; },
-                          (ty + iy - 1 + H) * PW + lx + ix - 1 + XH, wx, wy, wz, &r);
-      }
-    }
-    return r;
-  };
-
-#pragma unroll 1
-  for (int st = 0; st < nst; ++st) {
-    TOPT_STRESS_POINT(st * 3 + 51);
-    cp_wait<0>();
-    __syncthreads();
-    if (st + 1 < nst) load_stage(z0 + (st + 1) * K + H);
-    cp_commit();
-    const int zs = z0 + st * K;  // the stage's first plane
-    // the 4 points of this lane's column: displacement, floors, factor
-    float d[4][3], e[4];
-    int f[4][3];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const unsigned o = (unsigned)(st * K + k) * P32;
-      d[k][0] = __ldg(at_u32(pd, o));
-      d[k][1] = __ldg(at_u32(pd, F32 + o));
-      d[k][2] = __ldg(at_u32(pd, 2u * F32 + o));
-      e[k] = HAS_E ? __ldg(at_u32(pE, o)) : 1.0f;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) f[k][c] = (int)floorf(d[k][c]);
-    }
-    bool same = true;
-#pragma unroll
-    for (int k = 1; k < 4; ++k) same = same && f[k][0] == f[0][0] && f[k][1] == f[0][1] && f[k][2] == f[0][2];
-    const int ix = f[0][0], iy = f[0][1], iz = f[0][2];
-    bool ok = same && !(ix < -XH + 1 || ix > XH - 2 || iy < -H + 1 || iy > H - 2 || iz < -H + 1 || iz > H - 2);
-    int mn = __reduce_min_sync(0xffffffffu, ok ? ix : 1 << 20);
-    int mx = __reduce_max_sync(0xffffffffu, ok ? ix : -(1 << 20));
-    if (mx > mn + 1) {
-      // the ok lanes' x floors span more than two values: keep the two-value band [m, m + 1] that
-      // holds the most of them (floors are in [-3, 2]); the others join the queue
-      int best = -1, bm = mn;
-      for (int m = mn; m < mx; ++m) {
-        const int cnt = __popc(__ballot_sync(0xffffffffu, ok && (ix == m || ix == m + 1)));
-        if (cnt > best) {
-          best = cnt;
-          bm = m;
-        }
-      }
-      ok = ok && (ix == bm || ix == bm + 1);
-      mn = __reduce_min_sync(0xffffffffu, ok ? ix : 1 << 20);
-      mx = __reduce_max_sync(0xffffffffu, ok ? ix : -(1 << 20));
-    }
-    const bool w5 = mx == mn + 1;
-    if (__any_sync(0xffffffffu, ok) && ok) {
-      // weights: x as a W-vector at the lane-uniform column offset mn - 1 (W = 5 when the ok lanes'
-      // floors span two values, zero-padded), y and z as 4-vectors; points paired (0,1), (2,3)
-      float2 wx[2][5], wy[2][4], wz[2][4];
-#pragma unroll
-      for (int pr = 0; pr < 2; ++pr) {
-        float ax[4], bx[4], ay[4], by_[4], az[4], bz[4];
-        const int ka = 2 * pr, kb = ka + 1;
-        lag4(d[ka][0] - (float)ix, ax);
-        lag4(d[kb][0] - (float)ix, bx);
-        lag4(d[ka][1] - (float)iy, ay);
-        lag4(d[kb][1] - (float)iy, by_);
-        lag4(d[ka][2] - (float)iz, az);
-        lag4(d[kb][2] - (float)iz, bz);
-        const bool sh = w5 && ix != mn;
-#pragma unroll
-        for (int c = 0; c < 5; ++c)
-          wx[pr][c] = sh ? (c > 0 ? make_float2(ax[c - 1], bx[c - 1]) : make_float2(0.f, 0.f))
-                         : (c < 4 ? make_float2(ax[c], bx[c]) : make_float2(0.f, 0.f));
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          wy[pr][b] = make_float2(ay[b], by_[b]);
-          wz[pr][b] = make_float2(az[b], bz[b]);
-        }
-      }
-      // plane p (0..6) of the union = zs + iz - 1 + p; point k uses p = k .. k + 3
-      const int ro = (ty + iy - 1 + H) * PW + tx + mn - 1 + XH;
-      float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-      for (int p = 0; p < 7; ++p) {
-        const float* sp = sm + ((zs + iz - 1 + p) & (NZR - 1)) * PS + ro;
-        float2 pl[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          float sv[5];
-#pragma unroll
-          for (int c = 0; c < 5; ++c)
-            if (c < 4 || w5) sv[c] = sp[b * PW + c];
-#pragma unroll
-          for (int pr = 0; pr < 2; ++pr) {
-            if (p < 2 * pr || p > 2 * pr + 4) continue;  // pair (2pr, 2pr+1) spans planes 2pr .. 2pr+4
-            float2 row = __fmul2_rn(wx[pr][0], make_float2(sv[0], sv[0]));
-#pragma unroll
-            for (int c = 1; c < 5; ++c)
-              if (c < 4 || w5) row = __ffma2_rn(wx[pr][c], make_float2(sv[c], sv[c]), row);
-            pl[pr] = __ffma2_rn(wy[pr][b], row, pl[pr]);
-          }
-        }
-#pragma unroll
-        for (int pr = 0; pr < 2; ++pr) {
-          const int ka = 2 * pr;
-          if (p < ka || p > ka + 4) continue;
-          const float za = (p - ka >= 0 && p - ka <= 3) ? wz[pr][p - ka < 4 ? p - ka : 0].x : 0.0f;
-          const float zb = (p - ka - 1 >= 0 && p - ka - 1 <= 3) ? wz[pr][p - ka - 1 >= 0 ? p - ka - 1 : 0].y : 0.0f;
-          acc[pr] = __ffma2_rn(make_float2(za, zb), pl[pr], acc[pr]);
-        }
-      }
-      const float res[4] = {acc[0].x, acc[0].y, acc[1].x, acc[1].y};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) *at_u32(pout, (unsigned)(st * K + k) * P32) = HAS_E ? res[k] * e[k] : res[k];
-    }
-    // queue the points of the lanes that did not take the quad path; evaluate with full warps
-    const unsigned nok = __ballot_sync(0xffffffffu, !ok);
-    if (nok) {
-      // point-major order (entry k cnt + rank): a batch of consecutive entries comes from distinct
-      // lanes, so their columns fall in distinct banks (lane-major order put 4 planes of one column
-      // — one bank — side by side: 4-way conflicts)
-      const int cnt = __popc(nok), rank = __popc(nok & ((1u << tx) - 1u));
-      if (!ok) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int q = k * cnt + rank;
-          qcode[q] = (k << 5) | tx;
-          qdx[q] = d[k][0];
-          qdy[q] = d[k][1];
-          qdz[q] = d[k][2];
-          qE[q] = e[k];
-        }
-      }
-      __syncwarp();
-      const int total = 4 * __popc(nok);
-#pragma unroll 1
-      for (int q0 = 0; q0 < total; q0 += 32) {
-        const int q = q0 + tx;
-        const bool valid = q < total;
-        const int code = valid ? qcode[q] : 0;
-        const int lx = code & 31, k = code >> 5;
-        const float r = single(valid, lx, zs + k, valid ? qdx[q] : 0.f, valid ? qdy[q] : 0.f, valid ? qdz[q] : 0.f);
-        if (valid) {
-          const float v = HAS_E ? r * qE[q] : r;
-          pout[(size_t)(st * K + k) * plane + (lx - tx)] = v;
-        }
-      }
-      __syncwarp();
-    }
-  }
-  cp_wait<0>();
-}
-
-// =====================================================================================
 // Trace: both RK2 midpoint feet of the 3 velocity components (R6), fused sum of v.
 // =====================================================================================
 template <int HALO>
@@ -1039,21 +757,8 @@ static int resident_blocks(Kern k, int threads, size_t smem) {
   return (per_sm < 1 ? 1 : per_sm) * num_sms_sl();
 }
 
-template <bool HAS_E>
-static int launch_quad(const Geom& g, const TileArgs& a, cudaStream_t st) {
-  auto kern = k_sl_quad<HAS_E>;
-  static int resident = 0;
-  if (!resident) resident = resident_blocks(kern, 256, quad::SMEM);
-  const int zc = tiled_zc(g, pipe::H, pipe::K, resident);
-  const int blocks = (g.nx / tiled::TX) * (g.ny / tiled::TY) * (g.nz / zc);
-  kern<<<blocks, 256, quad::SMEM, st>>>(g, zc, a);
-  count_launch();
-  return blocks;
-}
-
 template <int MODE, bool HAS_E>
 static int launch_pipe(const Geom& g, const TileArgs& a, cudaStream_t st) {
-  if (TOPT_SL_QUAD && MODE == M_STEP) return launch_quad<HAS_E>(g, a, st);
   auto kern = k_sl_pipe<MODE, HAS_E>;
   static int resident = 0;
   if (!resident) resident = resident_blocks(kern, 256, pipe::SMEM);
