@@ -1255,9 +1255,119 @@ static void rx_inv_launch(const Geom& g, const ZList<C>& Z, const RealOut& out, 
   count_launch();
 }
 
+// TMA-staged form of the y / z passes without a spectral operator (k_rstrided MODE 0 forward,
+// MODE 1 inverse; one field per work item, in place): the N x TXC complex tile of the next item
+// arrives by one TMA tensor copy (3D map of the field, complex as 2 reals) while the current one is
+// transformed, into a two-slot ring; the tile doubles as the exchange scratch (interleaved,
+// swizzled).  128 threads, 32 KB of tiles: several blocks per SM.
+struct TmaZ {
+  CUtensorMap m[4];
+};
+constexpr int kRsThreads = 128;
+template <int N, int EMAX, int MODE, typename C>
+__global__ void __launch_bounds__(kRsThreads, 3) k_rstrided_tma(Geom g, int axis, const __grid_constant__ TmaZ tm,
+                                                                 ZList<C> Z, int nitems) {
+  static_assert(MODE == 0 || MODE == 1, "plain forward / inverse passes");
+  constexpr int E = Ev<N, EMAX>::v, T = N / E, TXC = kRsThreads / T;
+  constexpr int TILE = N * TXC;                // complex per tile
+  constexpr int BOX = N < 256 ? N : 256;
+  using Tr = typename Real<C>::T;
+  extern __shared__ __align__(128) unsigned char smr[];
+  C* tiles = reinterpret_cast<C*>(smr);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tiles + 2 * TILE);
+  const int c = threadIdx.x % TXC, t = threadIdx.x / TXC;
+  C tw[RfCfg<N, E>::NTW];
+  rf_twiddles<N, E>(tw, t);
+  const int tilesx = g.nx / TXC;
+  const int outerN = axis == 1 ? g.nz : g.ny;
+  const int tiles_per_field = tilesx * outerN;
+  const size_t Su = axis == 1 ? (size_t)g.nx : (size_t)g.nx * g.ny;
+  const int nmine = blockIdx.x < nitems ? (nitems - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  auto issue = [&](int k) {
+    const int item = blockIdx.x + k * gridDim.x;
+    const int tt = item % tiles_per_field, f = item / tiles_per_field;
+    const int x0 = (tt % tilesx) * TXC, outer = tt / tilesx;
+    C* dst = tiles + (k & 1) * TILE;
+    tma::mbar_arrive_expect_tx(bars + (k & 1), (unsigned)(TILE * sizeof(C)));
+    for (int p0 = 0; p0 < N; p0 += BOX)
+      tma::tensor4_g2s(dst + p0 * TXC, &tm.m[f], 2 * x0, axis == 1 ? p0 : outer, axis == 1 ? outer : p0, 0,
+                       bars + (k & 1));
+  };
+  if (threadIdx.x == 0) {
+    tma::mbar_init(bars, 1);
+    tma::mbar_init(bars + 1, 1);
+    tma::fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && nmine > 0) issue(0);
+  for (int k = 0; k < nmine; ++k) {
+    const int item = blockIdx.x + k * gridDim.x;
+    const int tt = item % tiles_per_field, f = item / tiles_per_field;
+    const int x0 = (tt % tilesx) * TXC, outer = tt / tilesx;
+    TOPT_STRESS_POINT(k * 3 + 61);
+    if (threadIdx.x == 0 && k + 1 < nmine) issue(k + 1);
+    tma::mbar_wait(bars + (k & 1), (unsigned)(k >> 1) & 1u);
+    C* tp = tiles + (k & 1) * TILE;
+    C a[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) a[e] = tp[(t + T * e) * TXC + c];
+    __syncthreads();  // the tile becomes the exchange scratch
+    rf_fft<N, E, MODE == 1, false, false, TXC>(a, tp + c, t, tw);
+    C* dstg = Z.z[f] + (axis == 1 ? ((size_t)outer << (g.lx + g.ly)) : ((size_t)outer << g.lx)) + x0 + c;
+#pragma unroll
+    for (int e = 0; e < E; ++e) dstg[(t + T * e) * Su] = a[e];
+    (void)sizeof(Tr);
+    TOPT_STRESS_POINT(k * 3 + 62);
+    __syncthreads();  // slot k&1 free for item k+2
+  }
+}
+
+#ifndef TOPT_RS_TMA
+#define TOPT_RS_TMA 1
+#endif
+template <typename C>
+static bool field_map(CUtensorMap* m, const C* base, const Geom& g, int axis, int box_x, int box_n) {
+  auto enc = tensor_map_encoder();
+  if (!enc || (((uintptr_t)base) & 15)) return false;
+  // complex as 2 reals: dims (2 nx, ny, nz, 1)
+  const CUtensorMapDataType dt = sizeof(C) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  const cuuint64_t es = sizeof(C) / 2;
+  const cuuint64_t dims[4] = {(cuuint64_t)2 * g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.nz, 1};
+  const cuuint64_t strides[3] = {(cuuint64_t)g.nx * sizeof(C), (cuuint64_t)g.nx * g.ny * sizeof(C),
+                                 (cuuint64_t)g.F * sizeof(C)};
+  const cuuint32_t box[4] = {(cuuint32_t)(2 * box_x), (cuuint32_t)(axis == 1 ? box_n : 1),
+                             (cuuint32_t)(axis == 1 ? 1 : box_n), 1u};
+  const cuuint32_t ones[4] = {1, 1, 1, 1};
+  (void)es;
+  return enc(m, dt, 4, const_cast<C*>(base), dims, strides, box, ones, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+template <int N, int EMAX, int MODE, typename C>
+static bool rstrided_tma_launch(const Geom& g, int axis, const ZList<C>& Z, int nin, cudaStream_t st) {
+  if constexpr (MODE > 1) {
+    return false;
+  } else {
+    constexpr int E = Ev<N, EMAX>::v, T = N / E, TXC = kRsThreads / T;
+    if (!TOPT_RS_TMA || N < 128 || N > 1024 || TXC < 2 || TXC * (int)sizeof(C) < 16 || g.nx % TXC || nin > 4)
+      return false;
+    TmaZ tm{};
+    for (int f = 0; f < nin; ++f)
+      if (!field_map(&tm.m[f], Z.z[f], g, axis, TXC, N < 256 ? N : 256)) return false;
+    const size_t sm = 2 * (size_t)N * TXC * sizeof(C) + 2 * sizeof(uint64_t);
+    const int outer = axis == 1 ? g.nz : g.ny;
+    const long long items = (long long)(g.nx / TXC) * outer * nin;
+    const int blocks = persistent_blocks(k_rstrided_tma<N, EMAX, MODE, C>, kRsThreads, sm, items);
+    k_rstrided_tma<N, EMAX, MODE, C><<<blocks, kRsThreads, sm, st>>>(g, axis, tm, Z, (int)items);
+    count_launch();
+    return true;
+  }
+}
+
 template <int N, int EMAX, int MODE, typename C>
 static void rstrided_launch(const Geom& g, int axis, const ZList<C>& Z, int nin, int nout, const SpecOp& op,
                             cudaStream_t st) {
+  if (MODE <= 1 && nin == nout && rstrided_tma_launch<N, EMAX, MODE, C>(g, axis, Z, nin, st)) return;
   constexpr int E = Ev<N, EMAX>::v, T = N / E;
   int TXC = kThreads / T;
   if (TXC > g.nx) TXC = g.nx;

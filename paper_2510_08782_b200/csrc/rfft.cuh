@@ -100,16 +100,18 @@ __device__ __forceinline__ void rf_sync() {
 // scratch addressing of the stage-boundary exchange: LS == 0 -> line[fft_pad(i)] (a padded line of
 // its own); LS > 0 -> line[i * LS] (lines interleaved with stride LS: a [position][line] tile, e.g. a
 // TMA-staged input tile reused as scratch once its values are in registers)
-// In the interleaved form a half-warp phase of 64-bit accesses holds 16 / LS positions; the radix-16
-// write pattern puts two of them 16 positions apart (same parity: same banks), so position i is
-// stored at i ^ bit4(i) — a bijection that gives the two different parities.
+// In the interleaved form a phase of a warp's accesses holds several positions of each column; the
+// first stage's writes put neighbouring threads' positions E apart (radix E: same parity, same
+// banks), so position i is stored at i ^ bit_log2(E)(i) — a bijection that gives them different
+// parities.  SH = log2(E).
 #ifndef TOPT_RF_SWZ
 #define TOPT_RF_SWZ 1
 #endif
-template <int LS>
+template <int LS, int SH>
 __device__ __forceinline__ int rf_idx(int i) {
-  return LS == 0 ? fft_pad(i) : (TOPT_RF_SWZ ? (i ^ ((i >> 4) & 1)) : i) * LS;
+  return LS == 0 ? fft_pad(i) : (TOPT_RF_SWZ ? (i ^ ((i >> SH) & 1)) : i) * LS;
 }
+__host__ __device__ constexpr int rf_log2(int e) { return e <= 1 ? 0 : 1 + rf_log2(e / 2); }
 
 template <int N, int E, int NS, int OFF, bool INV, bool WARP, bool FULL, int LS, typename C>
 __device__ __forceinline__ void rf_stage(C (&a)[E], C* line, int t, const C* tw) {
@@ -146,12 +148,12 @@ __device__ __forceinline__ void rf_stage(C (&a)[E], C* line, int t, const C* tw)
       const int j = t + b * T;
       const int base = (j / NS) * NS * R + (j & (NS - 1));
 #pragma unroll
-      for (int q = 0; q < R; ++q) line[rf_idx<LS>(base + q * NS)] = o[b + q * B];
+      for (int q = 0; q < R; ++q) line[rf_idx<LS, rf_log2(E)>(base + q * NS)] = o[b + q * B];
     }
     rf_sync<WARP>();
     TOPT_STRESS_POINT(NS * 17 + 2);
 #pragma unroll
-    for (int e = 0; e < E; ++e) a[e] = line[rf_idx<LS>(t + T * e)];
+    for (int e = 0; e < E; ++e) a[e] = line[rf_idx<LS, rf_log2(E)>(t + T * e)];
     rf_sync<WARP>();
     rf_stage<N, E, NS * R, OFF + (NS > 1 ? B * NB : 0), INV, WARP, FULL, LS, C>(a, line, t, tw);
   }

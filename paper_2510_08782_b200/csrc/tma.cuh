@@ -1,7 +1,8 @@
-// tma.cuh — Blackwell (sm_100a) bulk-copy staging: mbarrier transaction barriers and the TMA
-// bulk global->shared copy (cp.async.bulk ... mbarrier::complete_tx::bytes).  One elected warp
-// issues the copies of a stage; the consumers wait on the stage's mbarrier phase.  No register
-// staging, no per-thread address arithmetic for the fill, completion tracked in bytes.
+// tma.cuh — Blackwell (sm_100a) tile staging: mbarrier transaction barriers and the TMA tensor copy
+// global -> shared (cp.async.bulk.tensor ... mbarrier::complete_tx::bytes).  One thread issues the
+// copies of a stage; the consumers wait on the stage's mbarrier phase.  No register staging, no
+// per-thread address arithmetic for the fill, completion tracked in bytes.  (Plain cp.async.bulk row
+// copies of 128-160 bytes were measured slower than per-thread cp.async: DESIGN.md §7.)
 #pragma once
 #include <cstdint>
 
@@ -35,14 +36,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
-// TMA bulk copy of `bytes` (multiple of 16, 16-byte aligned ends) global -> shared, completing on `bar`
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
 // TMA tensor copy: the box at coordinates (c0..c3) of the 4D tensor map `tm` -> shared `dst`
 // (128-byte aligned), completing on `bar`
 __device__ __forceinline__ void tensor4_g2s(void* dst, const void* tm, int c0, int c1, int c2, int c3, uint64_t* bar) {

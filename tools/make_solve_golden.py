@@ -30,6 +30,9 @@ for a in (1e-2, 1e-3, 1e-4):
         CASES[f"c4_64_a{a:.0e}_w{w}"] = (4, (64, 64, 64), a, w, 1, 0)
 for p in (1, 2, 3, 4, 5):
     CASES[f"c3_128_p{p}"] = (3, (128, 128, 128), None, 5, 1, p - 1)
+# config 5's recipe (advection, H2, alpha = 1e-3, n_t = 16, w = 10) at 64^3 (its 512^3 oracle solve
+# would take days on the host)
+CASES["c5_64"] = (5, (64, 64, 64), None, 10, 1, 0)
 
 
 def run_case(name):
