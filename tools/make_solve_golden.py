@@ -33,6 +33,9 @@ for p in (1, 2, 3, 4, 5):
 # config 5's recipe (advection, H2, alpha = 1e-3, n_t = 16, w = 10) at 64^3 (its 512^3 oracle solve
 # would take days on the host)
 CASES["c5_64"] = (5, (64, 64, 64), None, 10, 1, 0)
+# config 4 at its native 256^3 (the benchmark's workload: continuity, H2, alpha = 1e-3, w = 5); hours of
+# host time, run with all cores: NUMBA_NUM_THREADS=8 python tools/make_solve_golden.py --jobs 1 --only c4_256
+CASES["c4_256"] = (4, (256, 256, 256), None, 5, 1, 0)
 
 
 def run_case(name):
