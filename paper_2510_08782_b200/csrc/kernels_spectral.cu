@@ -1151,6 +1151,9 @@ struct AsmArgs {
 #ifndef TOPT_ASM_MINB
 #define TOPT_ASM_MINB 2
 #endif
+#ifndef TOPT_ASM_TMA
+#define TOPT_ASM_TMA 1
+#endif
 template <int N, int LPR, bool LERAY>
 __global__ void __launch_bounds__(kThreads, TOPT_ASM_MINB) k_rassemble(Geom g, AsmArgs a, int ngroups) {
   constexpr int E = Ev<N, (LPR >= 4 ? 8 : 16)>::v, T = N / E, LPB = kThreads / T;
@@ -1166,17 +1169,52 @@ __global__ void __launch_bounds__(kThreads, TOPT_ASM_MINB) k_rassemble(Geom g, A
   float vbar[3] = {0.f, 0.f, 0.f};
   for (int c = 0; c < g.d; ++c) vbar[c] = a.vsum ? (float)(a.vsum[c] / a.ntot) : 0.f;
   double gmax = 0.0, sgs = 0.0, svu = 0.0, ssu = 0.0, sg[3] = {0, 0, 0}, ss[3] = {0, 0, 0};
+#if TOPT_ASM_TMA
+  // the group's LPR spectra (LPB consecutive rows each: one contiguous chunk per field) arrive by TMA
+  // bulk copies into one staging buffer, which is refilled with the NEXT group's rows as soon as
+  // this group's values are in registers — the copy overlaps the transforms and the combine
+  float2* stg = smem + LPB * R::STRIDE;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(stg + LPR * LPB * N);
+  const bool tma_on = nrows % LPB == 0;
+  auto issue = [&](int gq) {
+    tma::mbar_arrive_expect_tx(bar, (unsigned)(LPR * LPB * N * sizeof(float2)));
+#pragma unroll
+    for (int f = 0; f < LPR; ++f)
+      tma::bulk_g2s(stg + f * LPB * N, a.Z[f] + (size_t)gq * LPB * N, (unsigned)(LPB * N * sizeof(float2)), bar);
+  };
+  if (threadIdx.x == 0) {
+    tma::mbar_init(bar, 1);
+    tma::fence_mbar_init();
+  }
+  __syncthreads();
+  if (tma_on && threadIdx.x == 0 && (int)blockIdx.x < ngroups) issue(blockIdx.x);
+  unsigned phase = 0;
+#endif
   for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
     const size_t row = (size_t)grp * LPB + line;
     const bool ok = row < nrows;
     const size_t o = row * N + t;
     float2 z[LPR][E];
+#if TOPT_ASM_TMA
+    if (tma_on) {
+      tma::mbar_wait(bar, phase);
+      phase ^= 1u;
 #pragma unroll
-    for (int f = 0; f < LPR; ++f) {
+      for (int f = 0; f < LPR; ++f)
 #pragma unroll
-      for (int e = 0; e < E; ++e) z[f][e] = ok ? a.Z[f][o + T * e] : make_float2(0.f, 0.f);
-      rf_fft<N, E, true, WARP, true>(z[f], lbuf, t, tw);
+        for (int e = 0; e < E; ++e) z[f][e] = stg[(f * LPB + line) * N + t + T * e];
+      __syncthreads();  // every value is in registers: the buffer takes the next group
+      if (threadIdx.x == 0 && grp + (int)gridDim.x < ngroups) issue(grp + gridDim.x);
+    } else
+#endif
+    {
+#pragma unroll
+      for (int f = 0; f < LPR; ++f)
+#pragma unroll
+        for (int e = 0; e < E; ++e) z[f][e] = ok ? a.Z[f][o + T * e] : make_float2(0.f, 0.f);
     }
+#pragma unroll
+    for (int f = 0; f < LPR; ++f) rf_fft<N, E, true, WARP, true>(z[f], lbuf, t, tw);
     if (!ok) continue;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -1560,7 +1598,8 @@ void launch_bchain(const Geom& g, const float* b, float2* Zb, double alpha, int 
 template <int N, int LPR, bool LERAY>
 static void rassemble_launch(const Geom& g, const AsmArgs& a, int* nparts, cudaStream_t st) {
   constexpr int E = Ev<N, (LPR >= 4 ? 8 : 16)>::v, T = N / E, LPB = kThreads / T;
-  const size_t sm = (size_t)LPB * RfCfg<N, E>::STRIDE * sizeof(float2);
+  const size_t sm = (size_t)LPB * RfCfg<N, E, true>::STRIDE * sizeof(float2) +
+                    (TOPT_ASM_TMA ? (size_t)LPR * LPB * N * sizeof(float2) + sizeof(uint64_t) : 0);
   const size_t nrows = (size_t)g.ny * g.nz;
   const long long groups = (long long)((nrows + LPB - 1) / LPB);
   const int blocks = persistent_blocks(k_rassemble<N, LPR, LERAY>, kThreads, sm, groups);

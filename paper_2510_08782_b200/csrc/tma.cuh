@@ -36,6 +36,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
+// TMA bulk copy of `bytes` (multiple of 16, 16-byte aligned ends) global -> shared, completing on
+// `bar` — for LARGE contiguous chunks only (per-request cost dominates 128-byte rows)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 // TMA tensor copy: the box at coordinates (c0..c3) of the 4D tensor map `tm` -> shared `dst`
 // (128-byte aligned), completing on `bar`
 __device__ __forceinline__ void tensor4_g2s(void* dst, const void* tm, int c0, int c1, int c2, int c3, uint64_t* bar) {
