@@ -20,8 +20,10 @@ def f32(x):
 
 
 def case(config, n, scale=0.5, model=None, nt=None, alpha=None, reg_order=None):
-    """Seeded problem of `config`'s recipe on grid n; inputs rounded to fp32."""
-    d = make_problem(config, n)
+    """Seeded problem of `config`'s recipe on grid n; inputs rounded to fp32.  Grids of 256^3 and up
+    are generated on the GPU when one is present (the same closed forms, synth/phantoms.py)."""
+    big = int(np.prod(n)) >= 256 ** 3 and torch.cuda.is_available()
+    d = make_problem(config, n, device="cuda:0" if big else "cpu")
     if model is not None:
         d["model"] = model
     if nt is not None:
