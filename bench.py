@@ -148,6 +148,35 @@ def slab_of(field, rank, world, vector=False):
     return np.ascontiguousarray(field[..., z0:z0 + nzl, :, :])
 
 
+SLAB_CHECK_TOL = 1e-5  # north_star per-operator tolerance; emulated slabs agree to ~1e-7 (tests/test_gpu_slabs.py)
+SLAB_CHECK_KEYS = ("dist", "reg", "gs", "grad_inf")
+
+
+def slab_agreement(local, world, device=None, tol=SLAB_CHECK_TOL):
+    """z-slab evaluation vs the single-GPU evaluation of the WHOLE grid (bench.py at N > 1, once, before
+    timing).  `local` (per rank, from _slab_check): dl / rl = sums of squares of (g_slab - g_whole) and
+    g_whole over this rank's planes, sc_slab / sc_full = the global scalars of both evaluations (dicts
+    from Topt.scalars_dict), failed = 1.0 if this rank could not evaluate.  ONE all-reduce, the same
+    on every rank whatever failed, so a rank's failure cannot desynchronise the collectives.  Returns
+    the relative L2 of g over all slabs, the relative differences of dist, reg, <g,s>_h, ||g||_inf, ok."""
+    vals = [float(local.get("dl", 0.0)), float(local.get("rl", 0.0)), float(local.get("failed", 1.0))]
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor(vals, dtype=torch.float64, device=device)
+        dist.all_reduce(t)
+        vals = t.tolist()
+    dl, rl, failed = vals
+    if failed > 0:
+        return {"ok": False, "failed_ranks": int(round(failed)), **({"error": local["error"]} if "error" in local else {})}
+    out = {"g_rel_l2": (dl / rl) ** 0.5 if rl > 0 else dl ** 0.5}
+    for k in SLAB_CHECK_KEYS:  # global (all-reduced) scalars: the same on every rank
+        a, b = local["sc_slab"][k], local["sc_full"][k]
+        out[f"{k}_rel"] = abs(a - b) / max(abs(b), 1e-300)
+    out.update(tol=tol, ok=bool(max(out.values()) <= tol))
+    return out
+
+
 def max_over_ranks(x, world, device=None):
     """Max of a float over ranks (device time of the slowest rank)."""
     if world == 1:
@@ -271,6 +300,30 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _slab_check(t, topt, d, cfgp, dev, rank, world, m0n, m1n, vn):
+    """Evaluate once through the z-slab context t and once through a single-GPU context on the whole
+    grid (every rank, its own GPU); local sums for slab_agreement (no collective here)."""
+    import gc
+    import torch
+    f32 = lambda a: torch.tensor(a, dtype=torch.float32, device=dev)
+    m0, m1, v = f32(m0n), f32(m1n), f32(vn)
+    gs, ss, scs = torch.empty_like(v), torch.empty_like(v), torch.zeros(16, dtype=torch.float64, device=dev)
+    t.eval_gradient(m0, m1, v, gs, ss, scs)
+    sc_slab = t.scalars_dict(scs)
+    full = topt.Topt(topt.Config(window=d["window"], **cfgp), device=dev)
+    V = f32(d["vstar"])
+    gf, sf, scf = full.eval_gradient(f32(d["m0"]), f32(d["m1"]), V)
+    sc_full = full.scalars_dict(scf)
+    z0, nzl = slab_planes(V.shape[-3], rank, world)
+    gr = gf[..., z0:z0 + nzl, :, :].double()
+    res = {"dl": float(((gs.double() - gr) ** 2).sum()), "rl": float((gr ** 2).sum()),
+           "sc_slab": sc_slab, "sc_full": sc_full, "failed": 0.0}
+    del full, gf, sf, scf, V, gs, ss, gr
+    gc.collect()
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_topt(args):
     import numpy as np
     import torch
@@ -307,10 +360,24 @@ def run_topt(args):
         if t.transport != "p2p":  # agreed over the ranks inside topt_set_transport
             args.transport = "nccl"
             slab_error = slab_error or "p2p mapping failed on another rank"
+    zcheck = None
     if slab:
         m0n, m1n = slab_of(d["m0"], rank, world), slab_of(d["m1"], rank, world)
         vn = slab_of(d["vstar"], rank, world, vector=True)
-    else:
+        # once, before timing: this transport's z-slab evaluation against a single-GPU evaluation of
+        # the whole grid on every rank (g over all slabs and the global scalars); a mismatch falls back
+        # to replicas for the timed run and is recorded in the line
+        try:
+            local = _slab_check(t, topt, d, cfgp, dev, rank, world, m0n, m1n, vn)
+        except Exception as e:
+            local = {"failed": 1.0, "error": f"rank {rank}: {type(e).__name__}: {e}"[:200]}
+        zcheck = slab_agreement(local, world, dev)
+        if not zcheck["ok"]:  # the same verdict on every rank (one all-reduce)
+            slab, t = False, None
+            slab_error = slab_error or f"z-slab check failed: {zcheck}"[:300]
+            if rank == 0:
+                sys.stderr.write(f"bench: {slab_error}; running replicas\n")
+    if not slab:
         t = topt.Topt(topt.Config(window=d["window"], **cfgp), device=dev)
         m0n, m1n, vn = d["m0"], d["m1"], d["vstar"]
     m0 = torch.tensor(m0n, dtype=torch.float32, device=dev)
@@ -494,6 +561,7 @@ def run_topt(args):
                        "parallelism": (f"zslab{world}" if slab else f"replicas{world}") if world > 1 else "single",
                        **({"transport": args.transport} if slab else {}),
                        **({"zslab_error": slab_error} if slab_error else {}),
+                       **({"zslab_check": zcheck} if zcheck is not None else {}),
                        "l2": "inputs larger than L2 (~15 GB of HBM traffic per evaluation vs 126 MB L2)"},
             "clocks": clk.summary(),
             "e2e": e2e,

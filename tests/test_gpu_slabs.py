@@ -128,3 +128,21 @@ def test_solve_with_trial_feet_beyond_halo(P):
     assert (rp["obj_evals"], rp["grad_evals"], rp["rho"]) == (r1["obj_evals"], r1["grad_evals"], r1["rho"])
     assert abs(rp["obj"] - r1["obj"]) <= 1e-6 * abs(r1["obj"])
     assert rel_l2(host(vp), host(v1)) < 1e-5
+
+
+def test_bench_slab_check_on_emulated_slabs():
+    """bench.py's one-time z-slab check at N > 1 (_slab_check + slab_agreement), run here on an
+    emulated 4-slab context (all slabs in one process: rank 0 of a world of 1 owns the whole grid):
+    the z-slab and whole-grid evaluations must agree, and a g off by 1e-3 must fail the check."""
+    import torch
+
+    import bench
+    import paper_2510_08782_b200 as topt
+    from synth import make_problem
+    d = make_problem(2, (64, 32, 32))
+    cfgp = dict(n=tuple(d["n"]), nt=d["nt"], model=d["model"], reg_order=d["reg_order"], alpha=d["alpha"])
+    tp = topt.Topt(topt.Config(window=d["window"], **cfgp), device="cuda:0", world=4)
+    local = bench._slab_check(tp, topt, d, cfgp, torch.device("cuda:0"), 0, 1, d["m0"], d["m1"], d["vstar"])
+    res = bench.slab_agreement(local, 1)
+    assert res["ok"] and res["g_rel_l2"] < 1e-6, res
+    assert not bench.slab_agreement(dict(local, dl=local["rl"] * 1e-6), 1)["ok"]
