@@ -25,6 +25,7 @@ import os
 import statistics
 import subprocess
 import sys
+import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -71,24 +72,35 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        self.lines = []
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
+            return self
+        self.reader = threading.Thread(target=self._read, daemon=True)
+        self.reader.start()
+        t0 = time.time()  # the sampler is live before the timed region starts (short runs: >= 1 sample)
+        while not self.lines and time.time() - t0 < 5.0 and self.proc.poll() is None:
+            time.sleep(0.01)
         return self
 
+    def _read(self):
+        for l in self.proc.stdout:
+            if l.strip():
+                self.lines.append(l)
+
     def __exit__(self, *a):
-        self.lines = []
         if self.proc is not None:
             time.sleep(0.15)
             self.proc.terminate()
             try:
-                out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except Exception:
-                out = ""
-            self.lines = [l for l in out.splitlines() if l.strip()]
+                self.proc.kill()
+            self.reader.join(timeout=5)
 
     def summary(self):
         sm, smax, reasons = [], 0.0, set()
