@@ -101,7 +101,8 @@ typedef struct {
 typedef struct topt_ctx topt_ctx;
 
 /* Scalar outputs of an evaluation, written as fp64 to a DEVICE array of
- * TOPT_NSCALARS doubles (index names below). */
+ * TOPT_NSCALARS doubles (index names below; topt_eval_gradient writes the reserved slots
+ * 7..15 as zeros). */
 #define TOPT_NSCALARS 16
 enum {
   TOPT_S_OBJ = 0,      /* obj = dist + reg */
@@ -286,6 +287,16 @@ topt_status topt_linear_ngmres(topt_ctx* ctx, const float* b, double omega, floa
  * stream (adds event records; use a separate, un-timed pass).  Clears accumulated stats.
  * Synchronizes the device. */
 topt_status topt_profile(topt_ctx* ctx, int32_t enable);
+
+/* enable != 0 (the default): topt_eval_gradient and topt_objective replay CUDA graphs keyed by
+ * their pointer arguments (captured on first use; the workspace binding is baked in).  A single
+ * slab captures the whole evaluation; with z-slabs (world > 1, NCCL or emulated) topt_eval_gradient
+ * is captured in three segments between the host's two window decisions (max |v_z| before the trace, max |delta_z|
+ * after it), each segment keyed by the decisions before it; the NCCL calls are
+ * captured with the kernels (topt_objective runs eagerly on z-slabs).  enable == 0: every call runs eagerly (bitwise the same results).
+ * Per-rank setting, but the ranks must agree (the collectives are the same either way).
+ * Errors: TOPT_ERR_INVALID_ARG for a NULL ctx. */
+topt_status topt_set_graphs(topt_ctx* ctx, int32_t enable);
 
 /* Accumulated stats of kernel class `cls` (0..9; TOPT_ERR_INVALID_ARG past the end): class
  * name (static string), total event-timed ms, total ALGORITHMIC bytes (each operand read

@@ -298,6 +298,10 @@ class Topt:
     def profile(self, enable: bool = True):
         check(LIB.topt_profile(self.ctx, 1 if enable else 0), "topt_profile")
 
+    def set_graphs(self, enable: bool = True):
+        """CUDA-graph replay of evaluations (default on; z-slabs: segmented capture)."""
+        check(LIB.topt_set_graphs(self.ctx, 1 if enable else 0), "topt_set_graphs")
+
     def kernel_stats(self):
         """Per kernel class: name, event-timed ms, algorithmic bytes, launches (since profile())."""
         out = []

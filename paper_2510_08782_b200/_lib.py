@@ -87,6 +87,7 @@ SIGNATURES = {
     "topt_multidot": (_I, [_P, _P, ctypes.POINTER(_P), _I, _P, _P]),
     "topt_mix": (_I, [_P, _P, ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_double), _I, _P, _P]),
     "topt_profile": (_I, [_P, _I]),
+    "topt_set_graphs": (_I, [_P, _I]),
     "topt_kernel_stats": (_I, [_P, _I, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double),
                                ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]),
     "topt_launch_count": (ctypes.c_int64, []),

@@ -480,10 +480,10 @@ bool halo(topt_ctx* c, std::function<float*(Slab&)> base, int nf, size_t fstride
 }
 
 // ---- z-slab window sizing ("halo exchange sized from max|v|*dt"; P:136 no CFL cap)
-// max |x| over every slab's F floats of a(slab) and b(slab) (b may be null), all-reduced (max),
-// on the host: synchronises `st` (z-slabs only; a few microseconds per evaluation)
-double zmax(topt_ctx* c, std::function<const float*(Slab&)> a, std::function<const float*(Slab&)> b,
-            cudaStream_t st) {
+// Device part: max |x| over every slab's F floats of a(slab) and b(slab) (b may be null),
+// all-reduced (max) into slab 0's amaxd.
+void zmax_dev(topt_ctx* c, std::function<const float*(Slab&)> a, std::function<const float*(Slab&)> b,
+              cudaStream_t st) {
   std::vector<double*> slots;
   for (auto& sl : c->slabs) {
     cudaMemsetAsync(sl.amax, 0, sizeof(unsigned), st);
@@ -492,6 +492,9 @@ double zmax(topt_ctx* c, std::function<const float*(Slab&)> a, std::function<con
     slots.push_back(sl.amaxd);
   }
   comm_allreduce(c, slots, 1, true, st);
+}
+// Host part: read it (synchronises `st`; z-slabs only, a few microseconds per evaluation).
+double zmax_read(topt_ctx* c, cudaStream_t st) {
   double h = 0.0;
   cudaMemcpyAsync(&h, c->slabs[0].amaxd, sizeof(double), cudaMemcpyDeviceToHost, st);
   cudaStreamSynchronize(st);
@@ -517,6 +520,102 @@ Geom in_geom(const topt_ctx* c, const Slab& sl, int zw, bool wrap) {
   g.zh = zw;
   g.nzw = wrap ? c->nzg : 0;
   return g;
+}
+
+// The two window decisions of a z-slab evaluation as one integer (zw, wrap): point 0 sizes the
+// trace input from max |v_z| (the midpoint displacement dt/2 v_z/h_z is exact at the nodes),
+// point 1 the SL-step inputs from max |delta_z| over the feet.
+int window_code(int zw, bool wrap) { return 2 * zw + (wrap ? 1 : 0); }
+void window_of(int code, int& zw, bool& wrap) {
+  zw = code >> 1;
+  wrap = (code & 1) != 0;
+}
+int decision_of(const topt_ctx* c, double h, int point) {
+  const double D = point == 0 ? 0.5 * h * (double)c->slabs[0].g.cz : h;
+  int zw = 0;
+  bool wrap = false;
+  size_window(c, D, zw, wrap);
+  return window_code(zw, wrap);
+}
+
+// ---- segmented CUDA-graph capture of z-slab evaluations (P > 1) --------------------------
+const int kMaxGraphs = 32;
+const int kSlabSegs = 3;  // [v halo, max|v_z|] | [trace, max|delta_z|] | [rest of the evaluation]
+void seg_key(const void* key[8], const void* const base[6], int seg, const std::vector<int>& dec) {
+  key[0] = (const void*)(uintptr_t)(0x5e60 + seg);
+  for (int i = 0; i < 6; ++i) key[1 + i] = base[i];
+  uintptr_t d = 0;
+  for (size_t i = 0; i < dec.size() && (int)i < seg; ++i) d |= (uintptr_t)(dec[i] & 0xfffff) << (20 * i);
+  key[7] = (const void*)d;
+}
+topt_ctx::GraphEntry* find_graph(topt_ctx* c, const void* const key[8]) {
+  for (auto& ge : c->graphs)
+    if (std::equal(ge.key, ge.key + 8, key)) return &ge;
+  return nullptr;
+}
+void cache_graph(topt_ctx* c, const void* const key[8], cudaGraphExec_t exec, long long nlaunch) {
+  if (topt_ctx::GraphEntry* old = find_graph(c, key)) {
+    cudaGraphExecDestroy(old->exec);
+    old->exec = exec;
+    old->nlaunch = nlaunch;
+    return;
+  }
+  if ((int)c->graphs.size() >= kMaxGraphs) {
+    cudaGraphExecDestroy(c->graphs.front().exec);
+    c->graphs.erase(c->graphs.begin());
+  }
+  topt_ctx::GraphEntry ge;
+  std::copy(key, key + 8, ge.key);
+  ge.exec = exec;
+  ge.nlaunch = nlaunch;
+  c->graphs.push_back(ge);
+}
+// End the segment being captured on gcap (index = decisions taken so far): instantiate and
+// cache it, launch it on the user stream when `launch` (segments already replayed by this
+// evaluation are only re-cached), and unless `last` begin capturing the next segment.
+void seg_end(topt_ctx* c, bool launch, bool last) {
+  topt_ctx::SegCap& s = c->segc;
+  const int seg = (int)s.dec.size();
+  const long long nl = launch_count() - s.l0;
+  launch_count_add(-nl);  // captured, not launched
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  if (cudaStreamEndCapture(c->gcap, &graph) != cudaSuccess || !graph ||
+      cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess)
+    s.err = true;
+  if (graph) cudaGraphDestroy(graph);
+  if (!s.err) {
+    const void* key[8];
+    seg_key(key, s.base, seg, s.dec);
+    cache_graph(c, key, exec, nl);
+    if (launch) {
+      if (cudaGraphLaunch(exec, s.user) != cudaSuccess) s.err = true;
+      launch_count_add(nl);
+    }
+  }
+  s.l0 = launch_count();
+  if (!last && !s.err && cudaStreamBeginCapture(c->gcap, cudaStreamCaptureModeRelaxed) != cudaSuccess) s.err = true;
+}
+// One window decision (point 0 or 1) of a z-slab evaluation: the device part on `st`, then the
+// host read.  Under segmented capture the segment ends here: it is launched on the user stream
+// and the decision read there — or, for a segment this evaluation already replayed, the
+// decision it took is reused.
+int window_decision(topt_ctx* c, std::function<const float*(Slab&)> a, std::function<const float*(Slab&)> b,
+                    int point, cudaStream_t st) {
+  zmax_dev(c, a, b, st);
+  topt_ctx::SegCap& s = c->segc;
+  if (!s.on) return decision_of(c, zmax_read(c, st), point);
+  const size_t i = s.dec.size();
+  int d = 0;
+  if (i < s.known.size()) {
+    seg_end(c, false, false);
+    d = s.known[i];
+  } else {
+    seg_end(c, true, false);
+    d = s.err ? 0 : decision_of(c, zmax_read(c, s.user), point);
+  }
+  s.dec.push_back(d);
+  return d;
 }
 // Input of an interpolation over nf fields (field f of slab s at base(s) + f * fstride, halo'd
 // layout): the stored halo refreshed (zw == 0) or the window gathered into s.win from the LOCAL
@@ -661,9 +760,8 @@ void forward_half(topt_ctx* c, std::vector<Io>& io, bool want_adj, cudaStream_t 
         cudaMemcpyAsync(local(sl, sl.vh + a * sl.Fh), io[si].v + a * sl.F, sl.F * 4, cudaMemcpyDeviceToDevice, st);
     }
     // trace input: midpoint displacements dt/2 v_z/h_z at the nodes (exact, no interpolation)
-    const double Dv = 0.5 * zmax(c, [](Slab& s) { return (const float*)local(s, s.vh + 2 * s.Fh); }, nullptr, st) *
-                      (double)c->slabs[0].g.cz;
-    size_window(c, Dv, c->zw_v, c->wrap_v);
+    window_of(window_decision(c, [](Slab& s) { return (const float*)local(s, s.vh + 2 * s.Fh); }, nullptr, 0, st),
+              c->zw_v, c->wrap_v);
     sl_input(c, [](Slab& s) { return s.vh; }, c->d, c->slabs[0].Fh, c->zw_v, st);
   }
   for (size_t si = 0; si < c->slabs.size(); ++si) {
@@ -679,10 +777,11 @@ void forward_half(topt_ctx* c, std::vector<Io>& io, bool want_adj, cudaStream_t 
   }
   comm_allreduce(c, intls(io, I_SUMV), c->d, false, st);
   if (P > 1) {  // SL-step inputs: max |delta_z| over both feet
-    const double D = zmax(c, [](Slab& s) { return (const float*)s.df + 2 * s.F; },
-                          want_adj ? std::function<const float*(Slab&)>([](Slab& s) { return (const float*)s.da + 2 * s.F; })
-                                   : std::function<const float*(Slab&)>(), st);
-    size_window(c, D, c->zw_m, c->wrap_m);
+    window_of(window_decision(c, [](Slab& s) { return (const float*)s.df + 2 * s.F; },
+                              want_adj ? std::function<const float*(Slab&)>([](Slab& s) { return (const float*)s.da + 2 * s.F; })
+                                       : std::function<const float*(Slab&)>(),
+                              1, st),
+              c->zw_m, c->wrap_m);
   }
   const int zw = c->zw_m;
   const bool cont = c->p.model == TOPT_CONTINUITY;
@@ -1155,7 +1254,6 @@ extern "C" {
 // `body(stream)` is recorded on the library's capture stream (the caller's stream may be the
 // legacy default stream, which cannot capture), instantiated once and launched on `st`.
 // One slab only (no host decisions, no collectives); profiling mode runs eagerly.
-static const int kMaxGraphs = 16;
 static bool graphs_ok(topt_ctx* c) { return c->use_graphs && !c->prof && c->comm.P == 1; }
 static topt_status graph_run(topt_ctx* c, const void* const key[8], cudaStream_t st,
                              const std::function<topt_status(cudaStream_t)>& body) {
@@ -1198,6 +1296,61 @@ static topt_status graph_run(topt_ctx* c, const void* const key[8], cudaStream_t
   return TOPT_OK;
 }
 
+// z-slab evaluation (P > 1) through segmented graphs: replay segment k, read window decision k,
+// pick segment k+1 by it.  A missing segment re-runs the evaluation's host code under capture from
+// the start, reusing the decisions of the segments this evaluation already launched (those are
+// only re-cached).  NCCL collectives and point-to-point calls are captured like kernels.  A failed
+// capture switches slab graphs off for the context and the evaluation is re-run eagerly.
+static bool slab_graphs_ok(topt_ctx* c) { return c->use_graphs && !c->prof && c->comm.P > 1 && !c->slab_graphs_off; }
+static topt_status eval_slab_graphs(topt_ctx* c, std::vector<Io>& io, const void* const base[6], cudaStream_t st) {
+  std::vector<int> dec;
+  for (int seg = 0; seg < kSlabSegs; ++seg) {
+    const void* key[8];
+    seg_key(key, base, seg, dec);
+    topt_ctx::GraphEntry* ge = find_graph(c, key);
+    if (!ge) break;
+    TOPT_CUDA(cudaGraphLaunch(ge->exec, st));
+    launch_count_add(ge->nlaunch);
+    if (seg + 1 == kSlabSegs) {
+      window_of(dec[0], c->zw_v, c->wrap_v);
+      window_of(dec[1], c->zw_m, c->wrap_m);
+      return TOPT_OK;
+    }
+    dec.push_back(decision_of(c, zmax_read(c, st), seg));
+  }
+  if (!c->gcap) {
+    TOPT_CUDA(cudaStreamCreateWithFlags(&c->gcap, cudaStreamNonBlocking));
+    TOPT_CUDA(cudaEventCreateWithFlags(&c->ev_gcap, cudaEventDisableTiming));
+  }
+  topt_ctx::SegCap& sc = c->segc;
+  sc.err = false;
+  sc.user = st;
+  std::copy(base, base + 6, sc.base);
+  sc.known = dec;
+  sc.dec.clear();
+  sc.l0 = launch_count();
+  c->div_pending = c->u_pending = c->vf_pending = false;
+  if (cudaStreamBeginCapture(c->gcap, cudaStreamCaptureModeRelaxed) != cudaSuccess) sc.err = true;
+  if (!sc.err) {
+    sc.on = true;
+    forward_half(c, io, true, c->gcap);
+    backward_half(c, io, c->gcap);
+    if (!sc.err) seg_end(c, true, true);
+    sc.on = false;
+  }
+  if (!sc.err) return TOPT_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(c->gcap, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+    cudaGraph_t gr = nullptr;
+    cudaStreamEndCapture(c->gcap, &gr);
+    if (gr) cudaGraphDestroy(gr);
+  }
+  cudaStreamSynchronize(c->gcap);
+  cudaGetLastError();
+  c->slab_graphs_off = true;
+  return eval_gradient(c, io, st);
+}
+
 topt_status topt_eval_gradient(topt_ctx* c, const float* m0, const float* m1, const float* v, float* g, float* s,
                                double* d_scalars, void* stream) {
   topt_status s0 = need_ws(c);
@@ -1224,7 +1377,8 @@ topt_status topt_eval_gradient(topt_ctx* c, const float* m0, const float* m1, co
     io[0].s = s;
     io[0].scal = d_scalars;
   }
-  topt_status r = eval_gradient(c, io, st);
+  const void* base[6] = {m0, m1, v, g, s, d_scalars};
+  topt_status r = slab_graphs_ok(c) ? eval_slab_graphs(c, io, base, st) : eval_gradient(c, io, st);
   if (r != TOPT_OK) return r;
   if (emu(c)) {
     if (g) stage_vec_out(c, [](Slab& x) { return (const float*)x.gcur; }, g, st);
@@ -1599,6 +1753,13 @@ topt_status topt_profile(topt_ctx* c, int32_t enable) {
   c->recs.clear();
   for (int i = 0; i < 16; ++i) { c->pms[i] = 0.0; c->pbytes[i] = 0.0; c->plaunch[i] = 0; }
   c->prof = enable != 0;
+  return TOPT_OK;
+}
+
+topt_status topt_set_graphs(topt_ctx* c, int32_t enable) {
+  if (!c) return fail(TOPT_ERR_INVALID_ARG, "ctx is NULL");
+  c->use_graphs = enable != 0;
+  if (enable) c->slab_graphs_off = false;
   return TOPT_OK;
 }
 

@@ -111,6 +111,19 @@ struct topt_ctx {
   cudaStream_t gcap = nullptr;  // capture stream (the caller's may be the legacy stream)
   cudaEvent_t ev_gcap = nullptr;
   bool use_graphs = true;
+  // z-slab evaluations (P > 1) are captured in segments between the host's two window decisions
+  // (max |v_z| before the trace, max |delta_z| after it): segment k is keyed by the user pointers
+  // and the decisions 0..k-1; a replay launches segment k, reads decision k, picks segment k+1
+  struct SegCap {
+    bool on = false;            // capturing on gcap
+    bool err = false;           // a capture failed: slab graphs are switched off, the evaluation re-run
+    cudaStream_t user = nullptr;
+    const void* base[6]{};
+    std::vector<int> known;     // decisions already taken by this evaluation's replayed segments
+    std::vector<int> dec;       // decisions taken in this capture
+    long long l0 = 0;           // launch counter at the segment's start
+  } segc;
+  bool slab_graphs_off = false;
   // per-kernel-class timing (topt_profile / topt_kernel_stats)
   bool prof = false;
   struct Rec { int cls; cudaEvent_t a, b; double bytes; int launches; };

@@ -93,6 +93,7 @@ __global__ void k_finish(const double* __restrict__ isc, double* __restrict__ sc
   for (int c = 0; c < d; ++c) m += isc[I_SUMG + c] * isc[I_SUMS + c];
   sc[TOPT_S_SLS] = -cv * (isc[I_GS] - m / n);
   sc[TOPT_S_OBJ] = sc[TOPT_S_DIST] + sc[TOPT_S_REG];
+  for (int i = TOPT_S_SLS + 1; i < TOPT_NSCALARS; ++i) sc[i] = 0.0;  // reserved slots: defined zeros
 }
 void launch_finish(const double* isc, double* sc, int d, double n, double cellvol, cudaStream_t st) {
   k_finish<<<1, 1, 0, st>>>(isc, sc, d, n, cellvol);

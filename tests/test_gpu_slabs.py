@@ -146,3 +146,39 @@ def test_bench_slab_check_on_emulated_slabs():
     res = bench.slab_agreement(local, 1)
     assert res["ok"] and res["g_rel_l2"] < 1e-6, res
     assert not bench.slab_agreement(dict(local, dl=local["rl"] * 1e-6), 1)["ok"]
+
+
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_slab_graphs_equal_eager_bitwise(P, transport):
+    """z-slab evaluations replay CUDA graphs captured in three segments between the host's two
+    window decisions: bitwise the eager evaluation on first capture, on replay,
+    and when a new v changes the decisions (feet beyond the 4-plane halo: the window path, a new
+    segment captured while the earlier ones are replayed) and changes them back."""
+    import torch
+    d = case(2, (64, 32, 32), model=1)
+    wide = case(2, (64, 32, 32), model=1, scale=4.0)
+    vs = [dev(d["v"]), dev(d["v"]), dev(wide["v"]), dev(d["v"]), dev(wide["v"])]
+    m0, m1 = dev(d["m0"]), dev(d["m1"])
+    res = {}
+    for graphs in (False, True):
+        t = topt_for(d, world=P)
+        t.set_transport(transport)
+        t.set_graphs(graphs)
+        g = torch.empty_like(vs[0])
+        s = torch.empty_like(vs[0])
+        sc = torch.zeros(16, dtype=torch.float64, device=vs[0].device)
+        v = torch.empty_like(vs[0])  # one pointer key: the decisions alone pick the segments
+        out = []
+        for vk in vs:
+            v.copy_(vk)
+            l0 = t.launch_count()
+            t.eval_gradient(m0, m1, v, g, s, sc)
+            torch.cuda.synchronize()
+            out.append((host(g).copy(), host(s).copy(), host(sc).copy(), t.launch_count() - l0))
+        res[graphs] = out
+    for k, (a, b) in enumerate(zip(res[False], res[True])):
+        for x, y in zip(a[:3], b[:3]):
+            assert np.array_equal(x, y), k
+        assert a[3] == b[3] > 0, k  # replayed graphs count the kernels they contain
+    assert not np.array_equal(res[True][1][0], res[True][2][0])  # the wide v really differs
