@@ -541,6 +541,43 @@ __global__ void __launch_bounds__(256, 2) k_sl_trace(Geom g, int ZC, TileArgs a)
 // 250.  Otherwise the pair takes the per-point paths of k_sl_trace.  The 8-slot plane ring is
 // filled with cp.async, two planes per step, one barrier per pair.
 // =====================================================================================
+#ifndef TOPT_TRACE_MIRROR
+#define TOPT_TRACE_MIRROR 1  // mirrored-operand fast path of k_sl_trace2 (fewer FMAs, see below)
+#endif
+// Mirrored-operand form of a point's two midpoint stencils (k_sl_trace2 fast path).  On the
+// window nodes 0..4 (offsets -2..2) the adjoint weights a5 have support {1,2,3,e} (e = 4 when
+// the adjoint floor is 0, else 0) and the forward weights are a5 reversed (w_k(1-t) = w_{3-k}(t)).
+// So forward = sum_k a5[k] f[4-k] and adjoint = sum_k a5[k] f[k]: ONE scalar weight times the
+// operand pair (f[4-k], f[k]) gives both sides, with 4 terms per axis instead of the union
+// window's 5 packed ones.  x and y use this (the pair's two rows / columns are loaded per lane);
+// z keeps the packed (forward, adjoint) weights over the 5 window planes.
+struct MirrorW {
+  float ax[3], axe;  // a5_x[1..3], a5_x[e_x]
+  float ay[3], aye;  // a5_y[1..3], a5_y[e_y]
+  float2 wz[5];      // (a5_z[4-c], a5_z[c])
+};
+__device__ __forceinline__ void mirror_weights(const float cc[3], MirrorW& m) {
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    const float dA = 0.5f * cc[ax];
+    const float fA = floorf(dA);
+    float w[4];
+    lag4(dA - fA, w);
+    const bool sA = fA == 0.0f;
+    if (ax < 2) {
+      float* a = ax == 0 ? m.ax : m.ay;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) a[k] = sA ? w[k] : w[k + 1];
+      (ax == 0 ? m.axe : m.aye) = sA ? w[3] : w[0];
+    } else {
+      float a5[5];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) a5[k] = sA ? (k > 0 ? w[k - 1] : 0.0f) : (k < 4 ? w[k] : 0.0f);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) m.wz[k] = make_float2(a5[4 - k], a5[k]);
+    }
+  }
+}
 #ifndef TOPT_TRACE_MINB
 #define TOPT_TRACE_MINB 2
 #endif
@@ -648,6 +685,75 @@ __global__ void __launch_bounds__(256, TOPT_TRACE_MINB) k_sl_trace2(Geom g, int 
       if (f == 1) vs1 += (double)uA + (double)uB;
       if (f == 2) vs2 += (double)uA + (double)uB;
     }
+#if TOPT_TRACE_MIRROR
+    // the pair's x and y adjoint floors agree lane by lane (then both points read the same
+    // per-lane extra columns / rows): the mirrored-operand path
+    const bool sxA = floorf(0.5f * ccA[0]) == 0.0f, syA = floorf(0.5f * ccA[1]) == 0.0f;
+    const bool same = sxA == (floorf(0.5f * ccB[0]) == 0.0f) && syA == (floorf(0.5f * ccB[1]) == 0.0f);
+    if (__all_sync(0xffffffffu, ok && same)) {
+      MirrorW mA, mB;
+      mirror_weights(ccA, mA);
+      mirror_weights(ccB, mB);
+      // per-lane window offsets: extra column e_x / mirrored 4 - e_x, extra row e_y / 4 - e_y
+      const int cE = sxA ? 4 : 0, cM = 4 - cE;
+      const int rE = (syA ? 4 : 0) * PW, rM = 4 * PW - rE;
+#pragma unroll 1
+      for (int f = 0; f < NF; ++f) {
+        float2 resA = make_float2(0.f, 0.f), resB = resA;
+#pragma unroll
+        for (int cz = 0; cz < 6; ++cz) {  // window planes z-2 .. z+3
+          const float* pp = sm + (f * NZR + ((z - 2 + cz) & (NZR - 1))) * PS + rbase;
+          float r1[3], r2[3], r3[3], re[3], rm[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            r1[k] = pp[PW + 1 + k];
+            r2[k] = pp[2 * PW + 1 + k];
+            r3[k] = pp[3 * PW + 1 + k];
+            re[k] = pp[rE + 1 + k];
+            rm[k] = pp[rM + 1 + k];
+          }
+          const float r1e = pp[PW + cE], r1m = pp[PW + cM], r2e = pp[2 * PW + cE], r2m = pp[2 * PW + cM];
+          const float r3e = pp[3 * PW + cE], r3m = pp[3 * PW + cM], ree = pp[rE + cE], rmm = pp[rM + cM];
+          // Z_b = sum_k a5_x[k] (f[4-b][4-k], f[b][k]) for b = 1, 3, 2, e_y; plane = sum_b a5_y[b] Z_b
+          auto planev = [&](const MirrorW& m) -> float2 {
+            const float2 w1 = make_float2(m.ax[0], m.ax[0]), w2 = make_float2(m.ax[1], m.ax[1]);
+            const float2 w3 = make_float2(m.ax[2], m.ax[2]), we = make_float2(m.axe, m.axe);
+            float2 z1 = __fmul2_rn(w1, make_float2(r3[2], r1[0]));
+            z1 = __ffma2_rn(w2, make_float2(r3[1], r1[1]), z1);
+            z1 = __ffma2_rn(w3, make_float2(r3[0], r1[2]), z1);
+            z1 = __ffma2_rn(we, make_float2(r3m, r1e), z1);
+            float2 z3 = __fmul2_rn(w1, make_float2(r1[2], r3[0]));
+            z3 = __ffma2_rn(w2, make_float2(r1[1], r3[1]), z3);
+            z3 = __ffma2_rn(w3, make_float2(r1[0], r3[2]), z3);
+            z3 = __ffma2_rn(we, make_float2(r1m, r3e), z3);
+            float2 z2 = __fmul2_rn(w1, make_float2(r2[2], r2[0]));
+            z2 = __ffma2_rn(w2, make_float2(r2[1], r2[1]), z2);
+            z2 = __ffma2_rn(w3, make_float2(r2[0], r2[2]), z2);
+            z2 = __ffma2_rn(we, make_float2(r2m, r2e), z2);
+            float2 ze = __fmul2_rn(w1, make_float2(rm[2], re[0]));
+            ze = __ffma2_rn(w2, make_float2(rm[1], re[1]), ze);
+            ze = __ffma2_rn(w3, make_float2(rm[0], re[2]), ze);
+            ze = __ffma2_rn(we, make_float2(rmm, ree), ze);
+            float2 y = __fmul2_rn(make_float2(m.ay[0], m.ay[0]), z1);
+            y = __ffma2_rn(make_float2(m.ay[1], m.ay[1]), z2, y);
+            y = __ffma2_rn(make_float2(m.ay[2], m.ay[2]), z3, y);
+            return __ffma2_rn(make_float2(m.aye, m.aye), ze, y);
+          };
+          if (cz < 5) resA = __ffma2_rn(mA.wz[cz], planev(mA), resA);
+          if (cz > 0) resB = __ffma2_rn(mB.wz[cz - 1], planev(mB), resB);
+        }
+        const float sc = f == 0 ? g.cx : (f == 1 ? g.cy : g.cz);
+        if (a.out[0]) {
+          a.out[0][f * F + gA] = -1.0f * sc * resA.x;
+          a.out[0][f * F + gB] = -1.0f * sc * resB.x;
+        }
+        if (a.out[1]) {
+          a.out[1][f * F + gA] = 1.0f * sc * resA.y;
+          a.out[1][f * F + gB] = 1.0f * sc * resB.y;
+        }
+      }
+    } else
+#endif
     if (__all_sync(0xffffffffu, ok)) {
       float2 WA[3][5], WB[3][5];
       weights(ccA, WA);
