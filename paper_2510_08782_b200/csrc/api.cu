@@ -37,6 +37,11 @@ bool comm_window(topt_ctx* c, const std::vector<const float*>& src, size_t fs, i
 }  // namespace topt
 
 namespace {
+// Destroy every captured evaluation graph (workspace, transport or peer mappings changed).
+void drop_graphs(topt_ctx* c) {
+  for (auto& ge : c->graphs) cudaGraphExecDestroy(ge.exec);
+  c->graphs.clear();
+}
 
 thread_local std::string g_err;
 
@@ -281,8 +286,7 @@ topt_status topt_bind_workspace(topt_ctx* c, void* dptr, size_t bytes) {
   // peer mappings refer to the previous workspaces: transport 1 needs topt_set_peer_workspaces again
   c->comm.peer_ws.clear();
   c->comm.transport = 0;
-  for (auto& ge : c->graphs) cudaGraphExecDestroy(ge.exec);  // they bake the old workspace in
-  c->graphs.clear();
+  drop_graphs(c);  // they bake the old workspace in
   const int world = c->world;
   for (int si = 0; si < c->comm.nloc; ++si) {
     Slab& sl = c->slabs[si];
@@ -340,6 +344,7 @@ topt_status topt_set_transport(topt_ctx* ctx, int32_t transport) {
     const int mine = transport == 1 && (int)cm.peer_ws.size() == cm.P ? 1 : 0;
     transport = comm_agree_min(ctx, mine);
   }
+  if (ctx->comm.transport != transport) drop_graphs(ctx);  // captured z-slab segments bake the transport in
   ctx->comm.transport = transport;
   return TOPT_OK;
 }
@@ -350,9 +355,11 @@ topt_status topt_set_peer_workspaces(topt_ctx* ctx, void* const* bases, int32_t 
   if (!ctx) return fail(TOPT_ERR_INVALID_ARG, "NULL context");
   if (count == 0) {
     ctx->comm.peer_ws.clear();
+    drop_graphs(ctx);
     return TOPT_OK;
   }
   if (count != ctx->comm.P || !bases) return fail(TOPT_ERR_INVALID_ARG, "count must equal the world size");
+  drop_graphs(ctx);  // captured P2P segments bake the peer addresses in
   ctx->comm.peer_ws.assign(count, nullptr);
   for (int r = 0; r < count; ++r) ctx->comm.peer_ws[r] = static_cast<char*>(bases[r]);
   return TOPT_OK;

@@ -182,3 +182,35 @@ def test_slab_graphs_equal_eager_bitwise(P, transport):
             assert np.array_equal(x, y), k
         assert a[3] == b[3] > 0, k  # replayed graphs count the kernels they contain
     assert not np.array_equal(res[True][1][0], res[True][2][0])  # the wide v really differs
+
+
+def test_slab_graphs_follow_the_transport():
+    """Captured z-slab segments bake the transport in: switching it drops them, so the replayed
+    evaluation launches the new transport's kernels (the same count as the eager path)."""
+    import torch
+    d = case(2, (64, 32, 32), model=1)
+    m0, m1, v = dev(d["m0"]), dev(d["m1"]), dev(d["v"])
+
+    def launches(t):
+        g = torch.empty_like(v)
+        s = torch.empty_like(v)
+        sc = torch.zeros(16, dtype=torch.float64, device=v.device)
+        n = []
+        for _ in range(2):
+            l0 = t.launch_count()
+            t.eval_gradient(m0, m1, v, g, s, sc)
+            torch.cuda.synchronize()
+            n.append(t.launch_count() - l0)
+        return n
+
+    eager = {}
+    for tr in ("nccl", "p2p"):
+        t = topt_for(d, world=4)
+        t.set_transport(tr)
+        t.set_graphs(False)
+        eager[tr] = launches(t)[0]
+    assert eager["nccl"] != eager["p2p"]
+    t = topt_for(d, world=4)
+    for tr in ("nccl", "p2p", "nccl"):
+        t.set_transport(tr)
+        assert launches(t) == [eager[tr]] * 2, tr
