@@ -313,24 +313,32 @@ def run_reference(args):
 
 
 def _slab_check(t, topt, d, cfgp, dev, rank, world, m0n, m1n, vn):
-    """Evaluate once through the z-slab context t and once through a single-GPU context on the whole
-    grid (every rank, its own GPU); local sums for slab_agreement (no collective here)."""
+    """Evaluate once through the z-slab context t (eagerly, then twice through its segmented CUDA graphs,
+    which must reproduce the eager result bitwise: graphs_diff) and once through a single-GPU context on
+    the whole grid (every rank, its own GPU); local sums for slab_agreement (no collective here)."""
     import gc
     import torch
     f32 = lambda a: torch.tensor(a, dtype=torch.float32, device=dev)
     m0, m1, v = f32(m0n), f32(m1n), f32(vn)
     gs, ss, scs = torch.empty_like(v), torch.empty_like(v), torch.zeros(16, dtype=torch.float64, device=dev)
+    t.set_graphs(False)  # the eager z-slab evaluation first ...
     t.eval_gradient(m0, m1, v, gs, ss, scs)
     sc_slab = t.scalars_dict(scs)
+    ge, se, sce = gs.clone(), ss.clone(), scs.clone()
+    t.set_graphs(True)  # ... then its segmented CUDA graphs, captured and replayed: bitwise the same
+    same = True
+    for _ in range(2):
+        t.eval_gradient(m0, m1, v, gs, ss, scs)
+        same = same and torch.equal(gs, ge) and torch.equal(ss, se) and torch.equal(scs, sce)
     full = topt.Topt(topt.Config(window=d["window"], **cfgp), device=dev)
     V = f32(d["vstar"])
     gf, sf, scf = full.eval_gradient(f32(d["m0"]), f32(d["m1"]), V)
     sc_full = full.scalars_dict(scf)
     z0, nzl = slab_planes(V.shape[-3], rank, world)
     gr = gf[..., z0:z0 + nzl, :, :].double()
-    res = {"dl": float(((gs.double() - gr) ** 2).sum()), "rl": float((gr ** 2).sum()),
-           "sc_slab": sc_slab, "sc_full": sc_full, "failed": 0.0}
-    del full, gf, sf, scf, V, gs, ss, gr
+    res = {"dl": float(((ge.double() - gr) ** 2).sum()), "rl": float((gr ** 2).sum()),
+           "sc_slab": sc_slab, "sc_full": sc_full, "failed": 0.0, "graphs_diff": 0.0 if same else 1.0}
+    del full, gf, sf, scf, V, gs, ss, gr, ge, se, sce
     gc.collect()
     torch.cuda.empty_cache()
     return res
@@ -384,6 +392,10 @@ def run_topt(args):
         except Exception as e:
             local = {"failed": 1.0, "error": f"rank {rank}: {type(e).__name__}: {e}"[:200]}
         zcheck = slab_agreement(local, world, dev)
+        if zcheck["ok"]:  # graph replay of the z-slab evaluation: on unless a rank saw it differ from eager
+            gd = max_over_ranks(float(local.get("graphs_diff", 1.0)), world, dev)
+            t.set_graphs(gd == 0.0)
+            zcheck["graphs"] = "on" if gd == 0.0 else "off: replay differed from the eager evaluation"
         if not zcheck["ok"]:  # the same verdict on every rank (one all-reduce)
             slab, t = False, None
             slab_error = slab_error or f"z-slab check failed: {zcheck}"[:300]

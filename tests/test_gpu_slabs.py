@@ -145,6 +145,7 @@ def test_bench_slab_check_on_emulated_slabs():
     local = bench._slab_check(tp, topt, d, cfgp, torch.device("cuda:0"), 0, 1, d["m0"], d["m1"], d["vstar"])
     res = bench.slab_agreement(local, 1)
     assert res["ok"] and res["g_rel_l2"] < 1e-6, res
+    assert local["graphs_diff"] == 0.0  # segmented graph replay == eager, bitwise
     assert not bench.slab_agreement(dict(local, dl=local["rl"] * 1e-6), 1)["ok"]
 
 
