@@ -67,6 +67,39 @@ __device__ __forceinline__ void lag4(float t, float w[4]) {
   w[3] = fmaf(t, c6, c6);
 }
 
+// The same weights for two axes at once in packed fp32x2 (8 FFMA2/FMUL2 instead of 16 scalar
+// operations; identical IEEE roundings, so bitwise the scalar lag4's).
+__device__ __forceinline__ void lag4x2(float2 t, float2 w[4]) {
+  const float2 a = __ffma2_rn(t, t, make_float2(-t.x, -t.y));
+  const float2 c6 = __fmul2_rn(a, make_float2(1.0f / 6.0f, 1.0f / 6.0f));
+  const float2 c3 = __fmul2_rn(a, make_float2(1.0f / 3.0f, 1.0f / 3.0f));
+  const float2 h = __ffma2_rn(a, make_float2(0.5f, 0.5f), make_float2(-1.0f, -1.0f));
+  const float2 mt = make_float2(-t.x, -t.y);
+  w[0] = __ffma2_rn(mt, c6, c3);
+  w[1] = __ffma2_rn(t, h, make_float2(-h.x, -h.y));
+  w[2] = __fmul2_rn(mt, h);
+  w[3] = __ffma2_rn(t, c6, c6);
+}
+#ifndef TOPT_SL_PACKW
+#define TOPT_SL_PACKW 0  // packed x/y (trace: A/B) weights: measured no gain (SL step 1877 -> 1857 GB/s)
+#endif
+// x, y and z weights of one stencil (x and y packed)
+__device__ __forceinline__ void lag4_xyz(float tx, float ty, float tz, float wx[4], float wy[4], float wz[4]) {
+#if TOPT_SL_PACKW
+  float2 w[4];
+  lag4x2(make_float2(tx, ty), w);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    wx[k] = w[k].x;
+    wy[k] = w[k].y;
+  }
+#else
+  lag4(tx, wx);
+  lag4(ty, wy);
+#endif
+  lag4(tz, wz);
+}
+
 // base + idx (idx < 2^32 floats) as ONE mad.wide.u32 (the generic form costs a 32-bit add and
 // a 64-bit shift-add pair per address)
 template <typename T>
@@ -293,9 +326,7 @@ __global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, T
       const int mn = __reduce_min_sync(0xffffffffu, ix), mx = __reduce_max_sync(0xffffffffu, ix);
       if (mx == mn + 1 && __all_sync(0xffffffffu, inr)) {
         float wx[4], wy[4], wz[4];
-        lag4(dx - fx, wx);
-        lag4(dy - fy, wy);
-        lag4(dz - fz, wz);
+        lag4_xyz(dx - fx, dy - fy, dz - fz, wx, wy, wz);
         const bool sh = ix != mn;
         float w5[5];
 #pragma unroll
@@ -328,9 +359,7 @@ __global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, T
         r = gather_global(g, in, x0 + tx, y0 + ty, z, dx, dy, dz);
       } else {
         float wx[4], wy[4], wz[4];
-        lag4(dx - fx, wx);
-        lag4(dy - fy, wy);
-        lag4(dz - fz, wz);
+        lag4_xyz(dx - fx, dy - fy, dz - fz, wx, wy, wz);
         const int p0 = z + iz - 1;
         gather_smem<1, 0>(sm, [&](int c) { return ((p0 + c) & (NZR - 1)) * PS; },
                           (ty + iy - 1 + H) * PW + tx + ix - 1 + XH, wx, wy, wz, &r);
@@ -556,26 +585,43 @@ struct MirrorW {
   float ay[3], aye;  // a5_y[1..3], a5_y[e_y]
   float2 wz[5];      // (a5_z[4-c], a5_z[c])
 };
-__device__ __forceinline__ void mirror_weights(const float cc[3], MirrorW& m) {
+// axis `ax` of a point's MirrorW from its adjoint floor fA and lag4 weights w
+__device__ __forceinline__ void mirror_axis(float fA, const float w[4], int ax, MirrorW& m) {
+  const bool sA = fA == 0.0f;
+  if (ax < 2) {
+    float* a = ax == 0 ? m.ax : m.ay;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) a[k] = sA ? w[k] : w[k + 1];
+    (ax == 0 ? m.axe : m.aye) = sA ? w[3] : w[0];
+  } else {
+    float a5[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) a5[k] = sA ? (k > 0 ? w[k - 1] : 0.0f) : (k < 4 ? w[k] : 0.0f);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) m.wz[k] = make_float2(a5[4 - k], a5[k]);
+  }
+}
+// both points of a pair: the weights of A and B per axis in one packed lag4x2
+__device__ __forceinline__ void mirror_weights2(const float ccA[3], const float ccB[3], MirrorW& mA, MirrorW& mB) {
 #pragma unroll
   for (int ax = 0; ax < 3; ++ax) {
-    const float dA = 0.5f * cc[ax];
-    const float fA = floorf(dA);
-    float w[4];
-    lag4(dA - fA, w);
-    const bool sA = fA == 0.0f;
-    if (ax < 2) {
-      float* a = ax == 0 ? m.ax : m.ay;
+    const float dA = 0.5f * ccA[ax], dB = 0.5f * ccB[ax];
+    const float fA = floorf(dA), fB = floorf(dB);
+    float wA[4], wB[4];
+#if TOPT_SL_PACKW
+    float2 w[4];
+    lag4x2(make_float2(dA - fA, dB - fB), w);
 #pragma unroll
-      for (int k = 0; k < 3; ++k) a[k] = sA ? w[k] : w[k + 1];
-      (ax == 0 ? m.axe : m.aye) = sA ? w[3] : w[0];
-    } else {
-      float a5[5];
-#pragma unroll
-      for (int k = 0; k < 5; ++k) a5[k] = sA ? (k > 0 ? w[k - 1] : 0.0f) : (k < 4 ? w[k] : 0.0f);
-#pragma unroll
-      for (int k = 0; k < 5; ++k) m.wz[k] = make_float2(a5[4 - k], a5[k]);
+    for (int k = 0; k < 4; ++k) {
+      wA[k] = w[k].x;
+      wB[k] = w[k].y;
     }
+#else
+    lag4(dA - fA, wA);
+    lag4(dB - fB, wB);
+#endif
+    mirror_axis(fA, wA, ax, mA);
+    mirror_axis(fB, wB, ax, mB);
   }
 }
 #ifndef TOPT_TRACE_MINB
@@ -692,8 +738,7 @@ __global__ void __launch_bounds__(256, TOPT_TRACE_MINB) k_sl_trace2(Geom g, int 
     const bool same = sxA == (floorf(0.5f * ccB[0]) == 0.0f) && syA == (floorf(0.5f * ccB[1]) == 0.0f);
     if (__all_sync(0xffffffffu, ok && same)) {
       MirrorW mA, mB;
-      mirror_weights(ccA, mA);
-      mirror_weights(ccB, mB);
+      mirror_weights2(ccA, ccB, mA, mB);
       // per-lane window offsets: extra column e_x / mirrored 4 - e_x, extra row e_y / 4 - e_y
       const int cE = sxA ? 4 : 0, cM = 4 - cE;
       const int rE = (syA ? 4 : 0) * PW, rM = 4 * PW - rE;
