@@ -1015,27 +1015,36 @@ __global__ void __launch_bounds__(kThreads, TOPT_RZ_MINB) k_rzmerge(Geom g, int 
   // lines are transformed, so the strided HBM reads overlap the fp64 FFT work
   double2* Sv = reinterpret_cast<double2*>(smraw) + TXC * R::STRIDE;
   float2* Sb = reinterpret_cast<float2*>(Sv + N * TXC);
+  // TXC, tilesx and the tile count are powers of two: items and staging chunks decode by shifts.
+  // Chunk i of the staging tile is (row i / TXC, column i % TXC) for v (16-byte double2) and
+  // (row i / (TXC/2), columns 2 (i % (TXC/2)) + 0..1) for b; a thread's chunks are blockDim.x apart,
+  // i.e. a fixed number of rows, so its source pointer advances by a constant stride.
+  const int ltx = 31 - __clz(TXC), ltl = 31 - __clz(tilesx), lti = 31 - __clz(tiles);
+  const size_t vstep = (size_t)(blockDim.x >> ltx) * Su, bstep = (size_t)(blockDim.x >> (ltx - 1)) * Su;
+  const size_t voff = (size_t)(threadIdx.x >> ltx) * Su + (threadIdx.x & (TXC - 1));
+  const size_t boff = (size_t)(threadIdx.x >> (ltx - 1)) * Su + 2 * (threadIdx.x & (TXC / 2 - 1));
   auto stage = [&](int it) {
-    const int tt = it % tiles, f = it / tiles;
-    const int x0 = (tt % tilesx) * TXC, outer = tt / tilesx;
+    const int tt = it & (tiles - 1), f = it >> lti;
+    const int x0 = (tt & (tilesx - 1)) << ltx, outer = tt >> ltl;
     const unsigned t0 = (axis == 1 ? ((unsigned)outer << (g.lx + g.ly)) : ((unsigned)outer << g.lx)) + x0;
-    const double2* sv = Zv.z[f];
-    const float2* sb = Zb.z[f];
-    for (int i = threadIdx.x; i < N * TXC; i += blockDim.x) {
-      const int row = i / TXC, k = i % TXC;
-      cp_async16_f(Sv + row * TXC + k, reinterpret_cast<const float*>(sv + t0 + row * Su + k));
-    }
-    for (int i = threadIdx.x; i < N * TXC / 2; i += blockDim.x) {
-      const int row = i / (TXC / 2), k = i % (TXC / 2);
-      cp_async16_f(Sb + row * TXC + 2 * k, reinterpret_cast<const float*>(sb + t0 + row * Su + 2 * k));
-    }
+    const double2* sv = Zv.z[f] + t0 + voff;
+    const float2* sb = Zb.z[f] + t0 + boff;
+    for (int i = threadIdx.x; i < N * TXC; i += blockDim.x, sv += vstep)
+      cp_async16_f(Sv + i, reinterpret_cast<const float*>(sv));
+    for (int i = threadIdx.x; i < N * TXC / 2; i += blockDim.x, sb += bstep)
+      cp_async16_f(Sb + 2 * i, reinterpret_cast<const float*>(sb));
   };
   if ((int)blockIdx.x < nitems) stage(blockIdx.x);
   cp_commit_f();
 #endif
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+#if TOPT_RZ_PF
+    const int tt = item & (tiles - 1), f = item >> lti;
+    const int x0 = (tt & (tilesx - 1)) << ltx, outer = tt >> ltl;
+#else
     const int tt = item % tiles, f = item / tiles;
     const int x0 = (tt % tilesx) * TXC, outer = tt / tilesx;
+#endif
     const unsigned base = (axis == 1 ? ((unsigned)outer << (g.lx + g.ly)) : ((unsigned)outer << g.lx)) + x0 + c;
     const int qx = x0 + c;
     const double kx = qx <= g.nx / 2 ? qx : qx - g.nx;
