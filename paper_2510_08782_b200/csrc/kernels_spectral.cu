@@ -1177,7 +1177,9 @@ __global__ void __launch_bounds__(kThreads, TOPT_ASM_MINB) k_rassemble(Geom g, A
   constexpr int pf = LERAY ? LPR / 2 : 0;  // first p field
   float vbar[3] = {0.f, 0.f, 0.f};
   for (int c = 0; c < g.d; ++c) vbar[c] = a.vsum ? (float)(a.vsum[c] / a.ntot) : 0.f;
-  double gmax = 0.0, sgs = 0.0, svu = 0.0, ssu = 0.0, sg[3] = {0, 0, 0}, ss[3] = {0, 0, 0};
+  // |g|_inf in fp32 (a max of fp32 values is exact; one FMNMX instead of a convert + fp64 compare)
+  float gmax = 0.0f;
+  double sgs = 0.0, svu = 0.0, ssu = 0.0, sg[3] = {0, 0, 0}, ss[3] = {0, 0, 0};
 #if TOPT_ASM_TMA
   // the group's LPR spectra (LPB consecutive rows each: one contiguous chunk per field) arrive by TMA
   // bulk copies into one staging buffer, which is refilled with the NEXT group's rows as soon as
@@ -1246,7 +1248,7 @@ __global__ void __launch_bounds__(kThreads, TOPT_ASM_MINB) k_rassemble(Geom g, A
         const float sv = vbar[c] - vc + pc;
         if (a.g) a.g[gi] = gv;
         if (a.s) a.s[gi] = sv;
-        gmax = fmax(gmax, (double)fabsf(gv));
+        gmax = fmaxf(gmax, fabsf(gv));
         sgs += (double)(gv * sv);
         svu += (double)vc * uc;
         ssu += (double)sv * uc;
@@ -1255,7 +1257,7 @@ __global__ void __launch_bounds__(kThreads, TOPT_ASM_MINB) k_rassemble(Geom g, A
       }
     }
   }
-  double vals[10] = {gmax, sgs, svu, ssu, sg[0], sg[1], sg[2], ss[0], ss[1], ss[2]};
+  double vals[10] = {(double)gmax, sgs, svu, ssu, sg[0], sg[1], sg[2], ss[0], ss[1], ss[2]};
   __shared__ double sh[10][kThreads / 32];
   const int nw = (blockDim.x + 31) / 32;
 #pragma unroll
