@@ -637,6 +637,80 @@ static void rds_launch(const Geom& g, int axis, const DerivArgs& a, const DerivW
                                               a.out, (int)items);
 }
 
+// Single-field pass (div v: J = 1, no lam): k_rds with the next item's line elements (and the
+// accumulator it updates) loaded into registers while the current item is transformed — one item
+// holds too few bytes in flight to cover the HBM latency at two resident blocks per SM.
+#ifndef TOPT_RDS1
+#define TOPT_RDS1 1
+#endif
+template <int N>
+__global__ void __launch_bounds__(kThreads, 2) k_rds1(Geom g, int axis, int TXC, const float* __restrict__ psi,
+                                                   float w0, float beta, float* __restrict__ out, int nitems) {
+  constexpr int E = Ev<N, 8>::v, T = N / E;
+  using R = RfCfg<N, E>;
+  extern __shared__ __align__(16) float2 smem[];
+  const int c = threadIdx.x % TXC, t = threadIdx.x / TXC;
+  float2* lbuf = smem + c * R::STRIDE;
+  float2 tw[R::NTW];
+  rf_twiddles<N, E>(tw, t);
+  const int tilesx = g.nx / (2 * TXC);
+  const unsigned S = axis == 1 ? (unsigned)g.nx : (unsigned)g.nx * g.ny;
+  const float invN = 1.0f / (float)N;
+  auto base_of = [&](int item) -> unsigned {
+    const int x0 = (item % tilesx) * 2 * TXC, outer = item / tilesx;
+    return (axis == 1 ? ((unsigned)outer << (g.lx + g.ly)) : ((unsigned)outer << g.lx)) + x0 + 2 * c;
+  };
+  float2 zn[E], on[E];
+  auto fetch = [&](int item) {
+    const unsigned b = base_of(item);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      zn[e] = __ldg(reinterpret_cast<const float2*>(psi + b + (t + T * e) * S));
+      on[e] = beta != 0.0f ? *reinterpret_cast<const float2*>(out + b + (t + T * e) * S) : make_float2(0.f, 0.f);
+    }
+  };
+  if ((int)blockIdx.x < nitems) fetch(blockIdx.x);
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    float2 z[E], o[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      z[e] = zn[e];
+      o[e] = on[e];
+    }
+    if (item + (int)gridDim.x < nitems) fetch(item + gridDim.x);
+    rf_fft<N, E, false, false>(z, lbuf, t, tw);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const float k = kprime(t + T * e, N) * invN;
+      z[e] = make_float2(-k * z[e].y, k * z[e].x);
+    }
+    rf_fft<N, E, true, false>(z, lbuf, t, tw);
+    const unsigned b = base_of(item);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      float2 r = make_float2(fmaf(w0, z[e].x, 0.f), fmaf(w0, z[e].y, 0.f));
+      if (beta != 0.0f) {
+        r.x += beta * o[e].x;
+        r.y += beta * o[e].y;
+      }
+      *reinterpret_cast<float2*>(out + b + (t + T * e) * S) = r;
+    }
+  }
+}
+template <int N>
+static void rds1_launch(const Geom& g, int axis, const DerivArgs& a, const DerivWeights& w, cudaStream_t st) {
+  constexpr int E = Ev<N, 8>::v, T = N / E;
+  using R = RfCfg<N, E>;
+  int TXC = kThreads / T;
+  if (2 * TXC > g.nx) TXC = g.nx / 2;
+  const int threads = TXC * T;
+  const size_t sm = (size_t)TXC * R::STRIDE * sizeof(float2);
+  const int outer = axis == 1 ? g.nz : g.ny;
+  const long long items = (long long)(g.nx / (2 * TXC)) * outer;
+  const int blocks = persistent_blocks(k_rds1<N>, threads, sm, items);
+  k_rds1<N><<<blocks, threads, sm, st>>>(g, axis, TXC, a.psi, w.w[0], a.beta, a.out, (int)items);
+}
+
 template <int N>
 static void deriv_dispatch(const Geom& g, int axis, const DerivArgs& a, const DerivWeights& w, cudaStream_t st) {
   if (axis == 0) {
@@ -651,7 +725,12 @@ static void deriv_dispatch(const Geom& g, int axis, const DerivArgs& a, const De
                                             (int)groups);
   } else if (a.J == 1) {
     // single field (div v): the TMA-staged pass pipelines across work items; else occupancy first
-    if (!(TOPT_RDS_TMA_J1 && rds_tma_launch<N>(g, axis, a, w, st))) rds_launch<N, 8>(g, axis, a, w, st);
+    if (TOPT_RDS_TMA_J1 && rds_tma_launch<N>(g, axis, a, w, st)) {
+    } else if (TOPT_RDS1 && !a.lam) {
+      rds1_launch<N>(g, axis, a, w, st);
+    } else {
+      rds_launch<N, 8>(g, axis, a, w, st);
+    }
   } else {
     // time-slice sums: one smem exchange per FFT; at N >= 512 (one resident block per SM)
     // the tiles of the next slice are prefetched with cp.async (measured: +7% at 512^3,
