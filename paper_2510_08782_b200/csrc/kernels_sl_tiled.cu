@@ -202,6 +202,10 @@ namespace pipe {
 #define TOPT_SL_D 1
 #endif
 constexpr int H = TOPT_SL_HALO, K = TOPT_SL_K;  // y/z halo; planes per pipeline stage
+#ifndef TOPT_SL_JUNROLL
+#define TOPT_SL_JUNROLL 1
+#endif
+constexpr int JU = TOPT_SL_JUNROLL;             // unroll of the per-plane loop of a stage
 constexpr int D = TOPT_SL_D;                    // prefetch distance in stages (one barrier per stage)
 constexpr int NZR = 16;                         // ring slots (power of two)
 // the planes of stage st+D are copied at the top of stage st, over planes only stages < st need
@@ -302,7 +306,7 @@ __global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, T
     if (st + pipe::D < nst) load_stage(z0 + (st + pipe::D) * K + H);
     cp_commit();
     TOPT_STRESS_POINT(st * 3 + 12);
-#pragma unroll 1
+#pragma unroll pipe::JU
     for (int j = 0; j < K; ++j) {
       const int zi = st * K + j, z = z0 + zi;
       const unsigned o = (unsigned)zi * P32;
