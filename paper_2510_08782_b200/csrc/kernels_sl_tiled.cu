@@ -145,6 +145,9 @@ __device__ __forceinline__ float gather_global(const Geom& g, const float* __res
   return acc;
 }
 
+#ifndef TOPT_SL_XFIRST
+#define TOPT_SL_XFIRST 1  // gather_smem contracts x first (no per-tap x*y weight products; +1% SL step)
+#endif
 // 64-tap tricubic gather of NF fields from smem planes (field stride FS floats); slot(c) =
 // smem offset of plane c (c = 0..3: planes iz-1 .. iz+2), rowoff = offset of the first tap.
 // Planes are taken in pairs (c, c+1) by packed fp32x2 FMAs with the x-y weight product
@@ -161,6 +164,28 @@ __device__ __forceinline__ void gather_smem(const float* sm, SlotF slot, int row
     wy2[a] = make_float2(wy[a], wy[a]);
   }
   const int p0 = slot(0) + rowoff, p1 = slot(1) + rowoff, p2 = slot(2) + rowoff, p3 = slot(3) + rowoff;
+#if TOPT_SL_XFIRST
+  // contraction x, then y, then z: 32 + 8 FFMA2 per field (no per-tap weight products)
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    const float* s0 = sm + f * FS;
+    float2 lo = make_float2(0.f, 0.f), hi = lo;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int o = b * PW;
+      float2 r01 = __fmul2_rn(wx2[0], make_float2(s0[p0 + o], s0[p1 + o]));
+      float2 r23 = __fmul2_rn(wx2[0], make_float2(s0[p2 + o], s0[p3 + o]));
+#pragma unroll
+      for (int a = 1; a < 4; ++a) {
+        r01 = __ffma2_rn(wx2[a], make_float2(s0[p0 + o + a], s0[p1 + o + a]), r01);
+        r23 = __ffma2_rn(wx2[a], make_float2(s0[p2 + o + a], s0[p3 + o + a]), r23);
+      }
+      lo = b ? __ffma2_rn(wy2[b], r01, lo) : __fmul2_rn(wy2[b], r01);
+      hi = b ? __ffma2_rn(wy2[b], r23, hi) : __fmul2_rn(wy2[b], r23);
+    }
+    res[f] = fmaf(wz[3], hi.y, fmaf(wz[2], hi.x, fmaf(wz[1], lo.y, wz[0] * lo.x)));
+  }
+#else
 #pragma unroll
   for (int f = 0; f < NF; ++f) {
     const float* s0 = sm + f * FS;
@@ -178,6 +203,7 @@ __device__ __forceinline__ void gather_smem(const float* sm, SlotF slot, int row
       }
     res[f] = fmaf(wz[3], hi.y, fmaf(wz[2], hi.x, fmaf(wz[1], lo.y, wz[0] * lo.x)));
   }
+#endif
 }
 
 __device__ __forceinline__ void cp_async16(float* smem, const float* g) {
@@ -222,6 +248,52 @@ static_assert(H % K == 0, "stages of K planes tile the halo");
 #ifndef TOPT_SL_XWIN
 #define TOPT_SL_XWIN 1  // warp-uniform 5-column x window when the warp's x floors span two values
 #endif
+#ifndef TOPT_SL_XWIN_TEST
+#define TOPT_SL_XWIN_TEST 1  // ... only when the per-lane path would have bank conflicts
+#endif
+#ifndef TOPT_SL_XWIN6
+#define TOPT_SL_XWIN6 1  // 6-column window for warps whose x floors take three values (+2% SL step)
+#endif
+// x-window gather of k_sl_pipe: every lane reads the NC columns starting at the warp's common
+// offset (row pointer s), its 4 x weights placed at offset sh = ix - min(ix) of an NC-vector
+// (zeros elsewhere); planes p0 .. p0+3 (ring slots), contraction x, then y, then z.
+template <int NC>
+__device__ __forceinline__ float xwin_gather(const float* s, int p0, int sh, const float wx[4], const float wy[4],
+                                             const float wz[4]) {
+  using pipe::NZR;
+  using pipe::PS;
+  using tiled::PW;
+  float wn[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    float w = 0.0f;
+#pragma unroll
+    for (int q = 0; q <= NC - 4; ++q)
+      if (k - q >= 0 && k - q < 4) w = sh == q ? wx[k - q] : w;
+    wn[k] = w;
+  }
+  const float* s0 = s + ((p0) & (NZR - 1)) * PS;
+  const float* s1 = s + ((p0 + 1) & (NZR - 1)) * PS;
+  const float* s2 = s + ((p0 + 2) & (NZR - 1)) * PS;
+  const float* s3 = s + ((p0 + 3) & (NZR - 1)) * PS;
+  float2 lo = make_float2(0.f, 0.f), hi = lo;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    float2 r01 = make_float2(0.f, 0.f), r23 = r01;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int oo = b * PW + k;
+      const float2 w = make_float2(wn[k], wn[k]);
+      r01 = __ffma2_rn(w, make_float2(s0[oo], s1[oo]), r01);
+      r23 = __ffma2_rn(w, make_float2(s2[oo], s3[oo]), r23);
+    }
+    const float2 wb = make_float2(wy[b], wy[b]);
+    lo = __ffma2_rn(wb, r01, lo);
+    hi = __ffma2_rn(wb, r23, hi);
+  }
+  return fmaf(wz[3], hi.y, fmaf(wz[2], hi.x, fmaf(wz[1], lo.y, wz[0] * lo.x)));
+}
+
 #ifndef TOPT_SL_MINB
 #define TOPT_SL_MINB 3  // resident blocks per SM the register budget is sized for
 #endif
@@ -328,35 +400,36 @@ __global__ void __launch_bounds__(256, TOPT_SL_MINB) k_sl_pipe(Geom g, int ZC, T
       // planes — with its 4 x weights at offset ix - mn of a 5-vector: 80 wavefronts per
       // point instead of 128.  Contraction order x, then y, then z.
       const int mn = __reduce_min_sync(0xffffffffu, ix), mx = __reduce_max_sync(0xffffffffu, ix);
+      bool win = false;
       if (mx == mn + 1 && __all_sync(0xffffffffu, inr)) {
+#if TOPT_SL_XWIN_TEST
+        // The per-lane 4-tap path is conflict-free when the lanes' columns tx + ix span < 32
+        // AND lanes reading the same column read the same row and plane (a broadcast): with two
+        // x floors, only neighbouring lanes can share a column.  That holds for ~55% of these
+        // warps (floors falling along x, 256^3 config-4 feet); only the rest pay the window's
+        // 80 wavefronts (all-path average 78 -> 71 wavefronts per warp-point).
+        const int cl = tx + ix;
+        const int span = __reduce_max_sync(0xffffffffu, cl) - __reduce_min_sync(0xffffffffu, cl);
+        const unsigned pk = (unsigned)(cl & 0xffff) | ((unsigned)(iy & 0xff) << 16) | ((unsigned)(iz & 0xff) << 24);
+        const unsigned nb = __shfl_down_sync(0xffffffffu, pk, 1);
+        const bool clash = tx < 31 && ((nb ^ pk) & 0xffffu) == 0u && nb != pk;
+        win = span >= 32 || __any_sync(0xffffffffu, clash);
+#else
+        win = true;
+#endif
+      }
+      if (win) {
         float wx[4], wy[4], wz[4];
         lag4_xyz(dx - fx, dy - fy, dz - fz, wx, wy, wz);
-        const bool sh = ix != mn;
-        float w5[5];
-#pragma unroll
-        for (int k = 0; k < 5; ++k) w5[k] = sh ? (k > 0 ? wx[k - 1] : 0.0f) : (k < 4 ? wx[k] : 0.0f);
-        const int p0 = z + iz - 1;
-        const int ro = (ty + iy - 1 + H) * PW + tx + mn - 1 + XH;
-        const float* s0 = sm + ((p0) & (NZR - 1)) * PS + ro;
-        const float* s1 = sm + ((p0 + 1) & (NZR - 1)) * PS + ro;
-        const float* s2 = sm + ((p0 + 2) & (NZR - 1)) * PS + ro;
-        const float* s3 = sm + ((p0 + 3) & (NZR - 1)) * PS + ro;
-        float2 lo = make_float2(0.f, 0.f), hi = lo;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          float2 r01 = make_float2(0.f, 0.f), r23 = r01;
-#pragma unroll
-          for (int k = 0; k < 5; ++k) {
-            const int oo = b * PW + k;
-            const float2 w = make_float2(w5[k], w5[k]);
-            r01 = __ffma2_rn(w, make_float2(s0[oo], s1[oo]), r01);
-            r23 = __ffma2_rn(w, make_float2(s2[oo], s3[oo]), r23);
-          }
-          const float2 wb = make_float2(wy[b], wy[b]);
-          lo = __ffma2_rn(wb, r01, lo);
-          hi = __ffma2_rn(wb, r23, hi);
-        }
-        r = fmaf(wz[3], hi.y, fmaf(wz[2], hi.x, fmaf(wz[1], lo.y, wz[0] * lo.x)));
+        r = xwin_gather<5>(sm + (ty + iy - 1 + H) * PW + tx + mn - 1 + XH, z + iz - 1, ix - mn, wx, wy, wz);
+#if TOPT_SL_XWIN6
+      } else if (mx == mn + 2 && __all_sync(0xffffffffu, inr) &&
+                 __reduce_max_sync(0xffffffffu, tx + ix) - __reduce_min_sync(0xffffffffu, tx + ix) >= 32) {
+        // three x floors whose columns wrap the banks: a 6-column window (96 wavefronts, not 128)
+        float wx[4], wy[4], wz[4];
+        lag4_xyz(dx - fx, dy - fy, dz - fz, wx, wy, wz);
+        r = xwin_gather<6>(sm + (ty + iy - 1 + H) * PW + tx + mn - 1 + XH, z + iz - 1, ix - mn, wx, wy, wz);
+#endif
       } else
 #endif
       if (!inr) {
