@@ -1060,6 +1060,10 @@ __global__ void __launch_bounds__(kThreads, (MODE >= 4 ? 1 : 2)) k_rstrided(Geom
 #ifndef TOPT_RZ_MINB
 #define TOPT_RZ_MINB 2
 #endif
+#ifndef TOPT_RZ_DUAL
+#define TOPT_RZ_DUAL 0  // v and b forward transforms (and g, p inverse ones) in lock step (rf_fft2):
+                      // 264 B of spills, bchain 4.05 -> 3.91 TB/s (also at 1 block/SM); off
+#endif
 template <int N>
 __global__ void __launch_bounds__(kThreads, TOPT_RZ_MINB) k_rzmerge(Geom g, int axis, int TXC, ZList<double2> Zv,
                                                          ZList<float2> Zb, ZList<float2> Pp, SpecOp op, int nitems,
@@ -1080,6 +1084,12 @@ __global__ void __launch_bounds__(kThreads, TOPT_RZ_MINB) k_rzmerge(Geom g, int 
   constexpr int SF = (N == 256 && TOPT_RZ_FSTRIDE >= R::STRIDE) ? TOPT_RZ_FSTRIDE : R::STRIDE;
   static_assert(SF * sizeof(float2) <= R::STRIDE * sizeof(double2), "fp32 scratch inside the fp64 one");
   float2* lbf = reinterpret_cast<float2*>(smraw) + c * SF;
+#if TOPT_RZ_DUAL
+  // second fp32 scratch (its own region after the staging tiles) for the lock-step transforms
+  float2* lbf2 = reinterpret_cast<float2*>(reinterpret_cast<double2*>(smraw) + TXC * R::STRIDE +
+                                           (TOPT_RZ_PF ? N * TXC : 0)) +
+                 (TOPT_RZ_PF ? N * TXC : 0) + c * SF;
+#endif
   double2 twd[R::NTW];
   float2 twf[R::NTW];
   rf_twiddles<N, E>(twd, t);
@@ -1158,8 +1168,12 @@ __global__ void __launch_bounds__(kThreads, TOPT_RZ_MINB) k_rzmerge(Geom g, int 
       ab[e] = sb[base + (t + T * e) * Su];
     }
 #endif
+#if TOPT_RZ_DUAL
+    rf_fft2<N, E, false, false>(av, lbd, twd, ab, lbf2, twf, t);
+#else
     rf_fft<N, E, false, false>(av, lbd, t, twd);
     rf_fft<N, E, false, false>(ab, lbf, t, twf);
+#endif
     float2 gg[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -1177,8 +1191,12 @@ __global__ void __launch_bounds__(kThreads, TOPT_RZ_MINB) k_rzmerge(Geom g, int 
       const float mp = -(float)op.invn * __frcp_rn((float)(op.alpha * Lt));
       ab[e] = make_float2(ab[e].x * mp, ab[e].y * mp);
     }
+#if TOPT_RZ_DUAL
+    rf_fft2<N, E, true, false>(gg, lbf, twf, ab, lbf2, twf, t);
+#else
     rf_fft<N, E, true, false>(gg, lbf, t, twf);
     rf_fft<N, E, true, false>(ab, lbf, t, twf);
+#endif
     float2* dg = Zb.z[f];
     float2* dp = Pp.z[f];
 #pragma unroll
@@ -1212,6 +1230,7 @@ static void rzmerge_launch(const Geom& g, int axis, const ZList<double2>& Zv, co
   const int threads = TXC * T;
   size_t sm = (size_t)TXC * RfCfg<N, E>::STRIDE * sizeof(double2);
   if (TOPT_RZ_PF) sm += (size_t)N * TXC * (sizeof(double2) + sizeof(float2));  // staging tiles
+  if (TOPT_RZ_DUAL) sm += (size_t)TXC * (N == 256 && TOPT_RZ_FSTRIDE >= RfCfg<N, E>::STRIDE ? TOPT_RZ_FSTRIDE : RfCfg<N, E>::STRIDE) * sizeof(float2);
   const int outer = axis == 1 ? g.nz : g.ny;
   const long long items = (long long)(g.nx / TXC) * outer * nf;
   const int blocks = persistent_blocks(k_rzmerge<N>, threads, sm, items);

@@ -167,4 +167,86 @@ __device__ __forceinline__ void rf_fft(C (&a)[E], C* line, int t, const C* tw) {
   rf_stage<N, E, 1, 0, INV, WARP, FULL, LS, C>(a, line, t, tw);
 }
 
+// Two independent lines (possibly of different precisions) transformed in lock step: the same
+// stage sequence as rf_stage, both lines' butterflies between one pair of barriers (half the
+// barriers of two rf_fft calls, twice the independent work between them).  line1 / line2 are
+// disjoint scratch lines.
+template <int N, int E, int NS, int OFF, bool INV, bool WARP, bool FULL, int LS, typename C1, typename C2>
+__device__ __forceinline__ void rf_stage2(C1 (&a1)[E], C1* line1, const C1* tw1, C2 (&a2)[E], C2* line2,
+                                          const C2* tw2, int t) {
+  constexpr int R = rf_rad(N, E, NS), B = E / R, T = N / E, NB = rf_nb(R, FULL);
+  constexpr bool LAST = NS * R == N;
+  C1 o1[E];
+  C2 o2[E];
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    C1 x1[R];
+    C2 x2[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      x1[r] = a1[b + r * B];
+      x2[r] = a2[b + r * B];
+    }
+    if constexpr (NS > 1) {
+      C1 w1[R];
+      C2 w2[R];
+      if constexpr (FULL) {
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+          w1[r] = tw1[OFF + b * NB + r - 1];
+          w2[r] = tw2[OFF + b * NB + r - 1];
+        }
+      } else {
+        rf_powers<R>(tw1 + OFF + b * NB, w1);
+        rf_powers<R>(tw2 + OFF + b * NB, w2);
+      }
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        x1[r] = INV ? cmulconj(x1[r], w1[r]) : cmul(x1[r], w1[r]);
+        x2[r] = INV ? cmulconj(x2[r], w2[r]) : cmul(x2[r], w2[r]);
+      }
+    }
+    Dft<R, INV, C1>::run(x1);
+    Dft<R, INV, C2>::run(x2);
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      o1[b + q * B] = x1[q];
+      o2[b + q * B] = x2[q];
+    }
+  }
+  if constexpr (LAST) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      a1[e] = o1[e];
+      a2[e] = o2[e];
+    }
+  } else {
+    TOPT_STRESS_POINT(NS * 17 + 3);
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int j = t + b * T;
+      const int base = (j / NS) * NS * R + (j & (NS - 1));
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        line1[rf_idx<LS, rf_log2(E)>(base + q * NS)] = o1[b + q * B];
+        line2[rf_idx<LS, rf_log2(E)>(base + q * NS)] = o2[b + q * B];
+      }
+    }
+    rf_sync<WARP>();
+    TOPT_STRESS_POINT(NS * 17 + 4);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      a1[e] = line1[rf_idx<LS, rf_log2(E)>(t + T * e)];
+      a2[e] = line2[rf_idx<LS, rf_log2(E)>(t + T * e)];
+    }
+    rf_sync<WARP>();
+    rf_stage2<N, E, NS * R, OFF + (NS > 1 ? B * NB : 0), INV, WARP, FULL, LS>(a1, line1, tw1, a2, line2, tw2, t);
+  }
+}
+template <int N, int E, bool INV, bool WARP, bool FULL = false, int LS = 0, typename C1, typename C2>
+__device__ __forceinline__ void rf_fft2(C1 (&a1)[E], C1* line1, const C1* tw1, C2 (&a2)[E], C2* line2,
+                                        const C2* tw2, int t) {
+  rf_stage2<N, E, 1, 0, INV, WARP, FULL, LS>(a1, line1, tw1, a2, line2, tw2, t);
+}
+
 }  // namespace topt
