@@ -514,6 +514,44 @@ def run_topt(args):
         e2e = {"value": evals / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(4 * npts * (2 + len(d["n"]))),
                "d2h_bytes_per_step": int(4 * npts * len(d["n"]) + 16 * 8)}
+        # context for e2e (outside the timed region): this box's pinned-copy bandwidth for the same
+        # buffers, H2D of the step's inputs and D2H of g (plain torch copies), and the evaluations/s
+        # that the slower direction alone would allow
+        try:
+            bufs = [torch.empty_like(x, device=dev) for x in (m0h, m1h, vh)]
+            gd = torch.empty_like(vh, device=dev)
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c2 = torch.cuda.Event(enable_timing=True)
+            for _ in range(2):
+                c0.record(stream)
+                for b_, h_ in zip(bufs, (m0h, m1h, vh)):
+                    b_.copy_(h_, non_blocking=True)
+                c1.record(stream)
+                gh.copy_(gd, non_blocking=True)
+                c2.record(stream)
+                torch.cuda.synchronize()
+            h2d_s, d2h_s = c0.elapsed_time(c1) / 1e3, c1.elapsed_time(c2) / 1e3
+            # both directions at once, as in the streamed steady state (full-duplex PCIe; the host side
+            # may not sustain both at full rate)
+            so = torch.cuda.Stream(device=dev)
+            for _ in range(2):
+                so.wait_stream(stream)
+                c0.record(stream)
+                with torch.cuda.stream(so):
+                    gh.copy_(gd, non_blocking=True)
+                for b_, h_ in zip(bufs, (m0h, m1h, vh)):
+                    b_.copy_(h_, non_blocking=True)
+                stream.wait_stream(so)
+                c1.record(stream)
+                torch.cuda.synchronize()
+            dup_s = c0.elapsed_time(c1) / 1e3
+            e2e["pcie"] = {"h2d_GB/s": round(e2e["h2d_bytes_per_step"] / h2d_s / 1e9, 1),
+                           "d2h_GB/s": round(4 * npts * len(d["n"]) / d2h_s / 1e9, 1),
+                           "duplex_ms": round(dup_s * 1e3, 3),
+                           "copy_bound_evals/s_per_rank": round(1.0 / max(h2d_s, d2h_s, dup_s), 1)}
+            del bufs, gd
+        except Exception as e:  # context only: never fails the line
+            e2e["pcie"] = {"error": f"{type(e).__name__}"}
 
     # GA-NGMRES iterations (Armijo trials, Gram inner products, host LSQ,
     # mixing, stop test) on the same problem from v^0 = 0, after freeing the evaluation context
